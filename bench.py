@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 state-vector hot path (BASELINE.json configs[3]: N=29 random 2D register,
+per-atom detuning map, noiseless 1 us Rydberg pulse, dt = 10 ns -> 100 Krylov time steps).
+
+A bench *step* is one exact time step psi <- exp(-i dt H_k) psi (one rsv_expm_step: the fused
+Lanczos H.psi passes + Krylov combination + occupation reduction, and the host read of that
+step's occupations). Default: W=3 warm-up steps then K=97 timed steps = the whole 1 us pulse.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 29] [--diag fly|vec]
+
+value = H.psi products per second (whole job); ms_per_step; s_per_us_pulse; effective HBM
+GB/s (32 B per amplitude per H.psi: read psi, write H psi); roofline of the dominant kernel;
+e2e through the public API (evolve_sv) with host initial/final state; CPU baseline (C port of
+the reference's numba matvec, OpenMP on the host cores, bounded sample). Multi-GPU (torchrun):
+independent replicas per GPU (round 1: sharding by top qubits not yet wired), max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = None
+try:
+    with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+        BASELINE_METRIC = json.load(fh)["metric"]
+except Exception:  # pragma: no cover
+    BASELINE_METRIC = "H.psi/sec and effective HBM GB/s at N=29 (1 GPU)/N=33 (8 GPU); s per 1 us pulse"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle C port)
+def cpu_baseline(n, seconds=12.0, chunk_log2=None, steps=None, warmup=1):
+    """Time the C restatement of the reference's matvec (rydsim/_kernels.py:14) on the host cores.
+
+    Bounded sample: each timed unit computes H.psi on a contiguous 1/2^k slice of the output
+    (each element still reads all N partners across the full 2^n state). Returns H.psi/s.
+    """
+    import ctypes
+
+    import psutil
+
+    from oracle import build as obuild
+
+    lib = obuild.load()
+    dp = ctypes.POINTER(ctypes.c_double)
+    avail = psutil.virtual_memory().available
+    n_used = n
+    while n_used > 16 and (16 + 16 + 8) * (2 ** n_used) > 0.6 * avail:
+        n_used -= 1
+    dim = 2 ** n_used
+    psi = np.empty(2 * dim)
+    out = np.empty(2 * dim)
+    diag = np.empty(dim)
+    lib.svref_fill(2 * dim, psi.ctypes.data_as(dp), 1234)
+    from paper_2510_09813_b200 import interaction_matrix, workloads
+
+    reg, seq = workloads.config("random29", n_override=n_used)
+    u = np.ascontiguousarray(interaction_matrix(reg))
+    om, de = seq.step(50)
+    lib.svref_build_diagonal(n_used, np.ascontiguousarray(de).ctypes.data_as(dp), u.ctypes.data_as(dp),
+                             diag.ctypes.data_as(dp))
+    h = np.ascontiguousarray(0.5 * om)
+    if chunk_log2 is None:
+        chunk_log2 = max(0, n_used - 24)
+    chunk = dim >> chunk_log2
+    nchunks = 1 << chunk_log2
+
+    def run(i):
+        b0 = (i % nchunks) * chunk
+        lib.svref_matvec_range(n_used, psi.ctypes.data_as(dp), diag.ctypes.data_as(dp), h.ctypes.data_as(dp),
+                               out.ctypes.data_as(dp), b0, b0 + chunk)
+
+    for i in range(warmup):
+        run(i)
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        run(done)
+        done += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and done >= steps) or (steps is None and el >= seconds):
+            break
+    el = time.perf_counter() - t0
+    hpsi = done / nchunks
+    # scale to the requested N if the host could not hold it (per-element work grows ~N/n_used)
+    rate = hpsi / el
+    if n_used != n:
+        rate = rate * (2 ** n_used) / (2 ** n) * (n_used / n)
+    return {"value": rate, "unit": "H.psi/s", "cores": int(lib.svref_threads()), "kind": "port",
+            "sample": (f"C/OpenMP restatement of rydsim/_kernels.py:14 matvec at N={n_used}"
+                       + ("" if n_used == n else f" scaled to N={n}")
+                       + f", {done} slices of 2^{n_used - chunk_log2} outputs ({hpsi:.3f} H.psi) in {el:.1f} s"),
+            "elapsed_s": el, "n_used": n_used}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_setup(gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        pg = dist
+    return rank, world, local, pg
+
+
+def max_over_ranks(x, pg):
+    if pg is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, local, pg = dist_setup(args.gpus)
+    if rank != 0:
+        barrier(pg)
+        return 0
+    t0 = time.time()
+    steps = args.steps
+    res = cpu_baseline(args.n, steps=steps, warmup=args.warmup, chunk_log2=max(0, args.n - 24))
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": res["value"], "unit": "H.psi/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * res["elapsed_s"] / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
+        "config": {"workload": f"random{args.n}: N={args.n} random 2D register, per-atom detuning map, "
+                               "1 us pulse; one step = H.psi on a bounded output slice",
+                   "n_qubits": args.n},
+        "cpu_baseline": {"value": res["value"], "unit": "H.psi/s", "cores": res["cores"], "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": res["value"], "unit": "H.psi/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(line), flush=True)
+    barrier(pg)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def alg_bytes_per_launch(family, n, k_avg, diag):
+    amp = 2 ** n
+    if family == "lo":
+        return (32 + (8 if diag == "vec" else 0)) * amp          # read x (+diag), write u
+    if family == "mid":
+        return 48 * amp                                          # read x, u; write u
+    if family == "last":
+        return 64 * amp                                          # read x, u, s_{j-1}; write w_j
+    return (k_avg + 1) * 16 * amp                                # combine: read k basis vectors, write psi
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local, pg = dist_setup(args.gpus)
+    from paper_2510_09813_b200 import KrylovConfig, ObservableSpec, SvRunConfig, evolve_sv, interaction_matrix
+    from paper_2510_09813_b200 import workloads
+    from paper_2510_09813_b200.engine import SvEngine
+
+    n = args.n
+    reg, seq = workloads.config(args.workload, dt_ns=args.dt, n_override=n)
+    total_steps = args.warmup + args.steps
+    if total_steps > seq.step_count:
+        raise SystemExit(f"warmup+steps={total_steps} exceeds the {seq.step_count}-step pulse")
+    cfg = KrylovConfig(args.tol)
+    u = interaction_matrix(reg)
+    t_setup = time.time()
+    eng = SvEngine(n, u, diag=args.diag, max_krylov_dim=cfg.max_krylov_dim)
+    eng.set_observables([1 << q for q in range(n)])
+    plan = eng.pass_plan()
+    stream = torch.cuda.current_stream()
+
+    def do_step(k):
+        nxt = seq.step(k + 1) if k + 1 < seq.step_count else None
+        om, de = seq.step(k)
+        rep = eng.step(om, de, float(seq.dt_ns), cfg.tolerance, cfg.max_krylov_dim, cfg.norm_epsilon,
+                       next_params=nxt, observe=True)
+        occ = eng.observables()   # device -> host read of the step's result
+        return rep, occ
+
+    for k in range(args.warmup):
+        do_step(k)
+    torch.cuda.synchronize()
+    barrier(pg)
+    eng.set_profiling(True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    reps = []
+    for k in range(args.warmup, total_steps):
+        rep, occ = do_step(k)
+        reps.append(rep)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier(pg)
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, pg)
+    prof = eng.profile()
+    matvecs = sum(r.matvecs for r in reps)
+    iters = [r.iterations for r in reps]
+    substeps = sum(r.substeps for r in reps)
+    krylov_cap = eng.krylov_cap
+    final_occ = occ.tolist()
+
+    secs = ms / 1e3
+    value = world * matvecs / secs
+    ms_per_step = ms / args.steps
+    hbm_peak, peak_kind = peaks()
+    eff_gbs = world * matvecs * 32 * 2 ** n / secs / 1e9
+    # dominant kernel family by device time inside the timed region
+    fam = max(prof, key=lambda f: prof[f]["ms"])
+    launches = prof[fam]["launches"]
+    k_avg = float(np.mean(iters)) if iters else 1.0
+    avg_launch_ms = prof[fam]["ms"] / max(1, launches)
+    alg = alg_bytes_per_launch(fam, n, k_avg, args.diag)
+    achieved = alg / (avg_launch_ms / 1e3) / 1e9
+    kernel_launches = int(sum(v["launches"] for v in prof.values()))
+    pass_ms = {f: round(v["ms"], 3) for f, v in prof.items()}
+
+    # ---- e2e through the public API: host initial state in, host final state + occupations out
+    e2e = None
+    if not args.no_e2e:
+        del eng
+        torch.cuda.empty_cache()
+        host_in = torch.zeros(2 ** n, dtype=torch.complex128, pin_memory=True)
+        host_in[0] = 1.0
+        host_out = torch.empty(2 ** n, dtype=torch.complex128, pin_memory=True)
+        sub = type(seq)(seq.dt_ns, seq.omegas[:total_steps], seq.deltas[:total_steps], seq.dt_ns * total_steps)
+        torch.cuda.synchronize()
+        barrier(pg)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        res = evolve_sv(sub, reg, SvRunConfig(krylov=cfg, initial_state=host_in,
+                                              observables=(ObservableSpec("occupation", (), 1),),
+                                              diag=args.diag, allow_above_cap=True))
+        host_out.copy_(res.final_state, non_blocking=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1e3 * wall), pg)
+        mv = sum(r.matvecs for r in res.krylov_reports)
+        state_bytes = 16 * 2 ** n
+        e2e = {"value": world * mv / (e2e_ms / 1e3), "unit": "H.psi/s",
+               "h2d_bytes_per_step": int((state_bytes + 16 * n * total_steps) / total_steps),
+               "d2h_bytes_per_step": int((state_bytes + 8 * n * total_steps) / total_steps),
+               "steps": total_steps, "ms": e2e_ms,
+               "path": "paper_2510_09813_b200.evolve_sv(host initial state) + final state copied to pinned host"}
+        del res
+        torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(n, seconds=args.cpu_seconds)
+            cpu.pop("elapsed_s", None)
+            cpu.pop("n_used", None)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "H.psi/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC,
+            "value": value,
+            "unit": "H.psi/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "complex128 (f64)",
+            "data": "synthetic",
+            "config": {
+                "workload": f"{args.workload}: N={n} random 2D register (mean spacing 7 um, min 6 um, "
+                            "C6 = 2pi*862690), per-atom detuning map 0.6..1, Blackman Omega peak 3pi rad/us, "
+                            f"delta -6..6 rad/us, 1 us pulse, dt={args.dt} ns, Krylov tol {args.tol}",
+                "n_qubits": n, "dt_ns": args.dt, "pulse_steps": seq.step_count,
+                "timed_steps": f"{args.warmup + 1}..{total_steps}",
+                "diag": args.diag,
+                "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                "l2": "inputs larger than L2 (state = %.1f GB)" % (16 * 2 ** n / 1e9),
+                "pass_plan": plan,
+                "krylov_vectors_resident": krylov_cap,
+            },
+            "hbm_gbs_effective": eff_gbs,
+            "s_per_us_pulse": ms_per_step * seq.step_count / 1e3 * (1000.0 / (seq.dt_ns * seq.step_count)),
+            "krylov": {"iterations_mean": k_avg, "iterations_max": max(iters) if iters else 0,
+                       "matvecs": matvecs, "substeps": substeps},
+            "kernel_ms": pass_ms,
+            "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm_peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": None,
+                         "alg_bytes_per_launch": alg, "avg_launch_ms": avg_launch_ms},
+            "gpu_launches": kernel_launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "final_occupations": [round(x, 6) for x in final_occ],
+            "setup_s": round(time.time() - t_setup, 1),
+        }
+        print(json.dumps(line), flush=True)
+    barrier(pg)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=97)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=29)
+    ap.add_argument("--workload", default="random29")
+    ap.add_argument("--dt", type=int, default=10)
+    ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--diag", default="fly", choices=["fly", "vec"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("note: warm-up < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

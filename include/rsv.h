@@ -1,0 +1,122 @@
+/* rsv.h -- C ABI of the B200 state-vector hot path (libprefix "rsv_").
+ *
+ * Drop-in boundary for the reference's state-vector path (rydsim, Python):
+ * the reference's host API (rydsim/hamiltonian.py, rydsim/krylov.py, rydsim/sv.py,
+ * rydsim/observables.py) is mirrored in Python by paper_2510_09813_b200/, which
+ * binds exactly these symbols through ctypes. Plain pointers and sizes only.
+ * Vectors are device pointers to 2^N complex128 values (interleaved re, im),
+ * qubit i = bit i of the basis index (rydsim/hamiltonian.py:1-8).
+ *
+ * All functions return 0 on success and a negative code on failure; the
+ * message is available from rsv_last_error(). There is no CPU fallback:
+ * without a CUDA device every compute entry point fails with RSV_ERR_CUDA.
+ */
+#ifndef RSV_H
+#define RSV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSV_OK 0
+#define RSV_ERR_ARG (-1)
+#define RSV_ERR_CUDA (-2)
+#define RSV_ERR_STATE (-3)
+#define RSV_ERR_NOT_CONVERGED (-4)
+
+#define RSV_DIAG_FLY 1   /* diagonal computed on the fly from U and detunings */
+#define RSV_DIAG_VEC 2   /* precomputed float64 interaction diagonal vector + detunings */
+
+typedef struct rsv_context rsv_context;
+
+/* Mirrors rydsim.krylov.KrylovReport (krylov.py:47) plus diagnostics. */
+typedef struct {
+  int iterations;     /* Lanczos vectors used (largest over sub-steps) */
+  int converged;      /* 1 when the a-posteriori estimate met the tolerance */
+  double residual;    /* final estimate |beta_k [exp(-i tau T_k)]_{k,1}| */
+  double alpha0;      /* <v0|H|v0>: Rayleigh quotient of the input state (Energy observable) */
+  double norm_in;     /* ||psi|| of the input state */
+  int substeps;       /* >1 when the Krylov basis hit the HBM cap and the step was split */
+  int matvecs;        /* H.psi products issued */
+} rsv_krylov_report;
+
+int rsv_version(void);
+const char* rsv_last_error(void);
+int rsv_device_count(int* out);
+
+/* Context for one register of n_qubits with interaction matrix U (n x n, row-major, host).
+ * Replaces the state the reference keeps across evolve_sv (sv.py:80): interaction matrix
+ * (hamiltonian.py:66), the interaction diagonal (sv.py:116) and the Krylov workspace.
+ * stream: cudaStream_t (may be NULL = legacy default stream). */
+int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* stream, rsv_context** out);
+void rsv_destroy(rsv_context* ctx);
+int rsv_set_stream(rsv_context* ctx, void* stream);
+
+/* Bind caller-allocated (e.g. torch) device vectors: nslots >= 3 vectors of 2^n complex128.
+ * Slot layout: Krylov basis s_0..s_{nslots-2} (s_0 = state) and one work vector.
+ * The Krylov cap is nslots - 2 vectors; steps needing more are split (exactly) in time. */
+int rsv_bind_slots(rsv_context* ctx, void* const* slots, int nslots);
+/* Index of the bound slot currently holding the state (changes after every step). */
+int rsv_state_slot(rsv_context* ctx, int* out);
+/* Bind a caller-allocated device buffer of 2^n float64 used as the diagonal vector:
+ * if fill_interaction != 0 it is filled with sum_{i<j} U_ij n_i n_j (sv.py:116),
+ * otherwise the caller's contents are used as an explicit diagonal (HamiltonianSlice.diagonal). */
+int rsv_bind_diag_vector(rsv_context* ctx, double* dev_diag, int fill_interaction);
+/* Full 2^n diagonal -sum delta_i n_i + sum_{i<j} U_ij n_i n_j into a device buffer
+ * (rydsim/hamiltonian.py:114 build_diagonal). Not used by the hot path (diag on the fly). */
+int rsv_build_diagonal(rsv_context* ctx, const double* deltas, double* dev_out);
+/* The state changed outside rsv (new initial state): invalidate cached per-state scalars. */
+int rsv_state_modified(rsv_context* ctx);
+
+/* H.psi, rydsim/hamiltonian.py:164 apply_hamiltonian (+ _kernels.py:14):
+ * out = diag(deltas, U) psi + sum_i omegas_i/2 X_i psi. psi and out are device
+ * pointers; they may alias only when n <= 12 (single pass). omegas, deltas: host
+ * arrays of n values (rad/us). Asynchronous on the context stream. */
+int rsv_apply_hamiltonian(rsv_context* ctx, const double* omegas, const double* deltas,
+                          const void* psi, void* out);
+
+/* One exact step psi <- exp(-i dt 1e-3 H) psi on the resident state
+ * (rydsim/krylov.py:67 expm_multiply with the matvec of sv.py:125-128).
+ * next_omegas/next_deltas (may be NULL): the following step's parameters, used to
+ * pre-reduce that step's first Lanczos scalar inside the Krylov combination.
+ * observe != 0 evaluates the masks set by rsv_set_observables on the new state. */
+int rsv_expm_step(rsv_context* ctx, const double* omegas, const double* deltas, double dt_ns,
+                  double tolerance, int max_krylov_dim, double norm_epsilon,
+                  const double* next_omegas, const double* next_deltas, int observe,
+                  rsv_krylov_report* report);
+
+/* Observables as bit masks M: value = sum_b |psi_b|^2 [b & M == M] / sum_b |psi_b|^2.
+ * occupation(q): M = 1<<q (observables.py:82); correlation(i,j): M = (1<<i)|(1<<j)
+ * (observables.py:102). */
+int rsv_set_observables(rsv_context* ctx, const uint64_t* masks, int nmask);
+int rsv_get_observables(rsv_context* ctx, double* out_host);
+/* Evaluate the masks on the resident state now (blocking). */
+int rsv_measure(rsv_context* ctx, double* out_host, double* norm_sq);
+
+/* Same masks on an arbitrary device vector psi (read-only), e.g. observables.occupations(). */
+int rsv_observe(rsv_context* ctx, const void* psi, const uint64_t* masks, int nmask, double* out_host,
+                double* norm_sq);
+/* sum_b |x_b - y_b|^2 (observables.py:137 norm_difference, computed without cancellation). */
+int rsv_diff_norm_sq(rsv_context* ctx, const void* x, const void* y, uint64_t n, double* out);
+
+/* Generic vector kernels for the callable-matvec Lanczos (krylov.py:96-121). */
+int rsv_zdotc(rsv_context* ctx, const void* x, const void* y, uint64_t n, double* out_re_im);
+int rsv_lanczos_update(rsv_context* ctx, void* w, const void* v, const void* vprev, double alpha,
+                       double beta, uint64_t n, double* out_norm_sq);
+int rsv_axpy(rsv_context* ctx, void* y, const void* x, double a_re, double a_im, uint64_t n);
+int rsv_scale(rsv_context* ctx, void* y, const void* x, double a_re, double a_im, uint64_t n);
+
+/* Introspection / measurement support. */
+int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* per pass: a, p, g, kind */
+int rsv_set_profiling(rsv_context* ctx, int on);
+/* per kernel family: [0]=lo pass, [1]=mid passes, [2]=last pass, [3]=combine; ms and launches */
+int rsv_get_profile(rsv_context* ctx, double* ms4, long long* launches4);
+int rsv_reset_profile(rsv_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSV_H */

@@ -1,0 +1,95 @@
+/* TEST INFRASTRUCTURE ONLY -- plain-C restatement of the reference's compiled CPU hot loop.
+ *
+ * Used solely as the timed CPU baseline (bench.py cpu_baseline / --impl reference).
+ * The product never links this file.
+ *
+ * svref_matvec restates rydsim/_kernels.py:14 (matvec_bitflip_diag, the numba
+ * kernel the reference dispatches to for N >= 10, hamiltonian.py:180-187):
+ *     out[b] = diag[b] * psi[b] + sum_i half_omega[i] * psi[b ^ (1 << i)]
+ * with the same per-element arithmetic, parallelised over b with OpenMP
+ * (element results do not depend on evaluation order across b).
+ * svref_build_diagonal restates hamiltonian.py:83-122 (doubling construction).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int svref_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void svref_matvec(int n, const double* psi, const double* diag, const double* half_omega, double* out) {
+  const int64_t dim = (int64_t)1 << n;
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < dim; ++b) {
+    double re = diag[b] * psi[2 * b];
+    double im = diag[b] * psi[2 * b + 1];
+    for (int i = 0; i < n; ++i) {
+      const double c = half_omega[i];
+      if (c != 0.0) {
+        const int64_t p = b ^ ((int64_t)1 << i);
+        re += c * psi[2 * p];
+        im += c * psi[2 * p + 1];
+      }
+    }
+    out[2 * b] = re;
+    out[2 * b + 1] = im;
+  }
+}
+
+/* Same arithmetic on the output range [b0, b1): a bounded sample of one H.psi
+ * (each element still reads all of its N partners across the whole vector). */
+void svref_matvec_range(int n, const double* psi, const double* diag, const double* half_omega, double* out,
+                        int64_t b0, int64_t b1) {
+#pragma omp parallel for schedule(static)
+  for (int64_t b = b0; b < b1; ++b) {
+    double re = diag[b] * psi[2 * b];
+    double im = diag[b] * psi[2 * b + 1];
+    for (int i = 0; i < n; ++i) {
+      const double c = half_omega[i];
+      if (c != 0.0) {
+        const int64_t p = b ^ ((int64_t)1 << i);
+        re += c * psi[2 * p];
+        im += c * psi[2 * p + 1];
+      }
+    }
+    out[2 * b] = re;
+    out[2 * b + 1] = im;
+  }
+}
+
+/* d[b] = -sum_i delta_i bit_i(b) + sum_{i<j} U_ij bit_i bit_j (row-major U, n x n). */
+void svref_build_diagonal(int n, const double* deltas, const double* u, double* out) {
+  const int64_t dim = (int64_t)1 << n;
+  out[0] = 0.0;
+  int64_t half = 1;
+  for (int k = 0; k < n; ++k) {
+    /* extending by qubit k: the bit_k = 1 half adds -delta_k + sum_{i<k} U_ik bit_i */
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < half; ++b) {
+      double add = -deltas[k];
+      for (int i = 0; i < k; ++i)
+        if ((b >> i) & 1) add += u[(int64_t)i * n + k];
+      out[half + b] = out[b] + add;
+    }
+    half <<= 1;
+  }
+  (void)dim;
+}
+
+void svref_fill(int64_t count, double* x, uint64_t seed) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < count; ++i) {
+    uint64_t z = seed + (uint64_t)i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[i] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}

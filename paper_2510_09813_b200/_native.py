@@ -1,0 +1,125 @@
+"""ctypes binding of the C ABI in ``include/rsv.h`` (the in-tree ``_rsv.so``).
+
+The product path has no CPU fallback: importing works without a GPU (so the
+CPU test-suite can check the exported symbols), but every compute call fails
+loudly when the extension or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import RydsimError, SolverError, ValidationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_rsv.so")
+
+RSV_OK = 0
+RSV_ERR_ARG = -1
+RSV_ERR_CUDA = -2
+RSV_ERR_STATE = -3
+RSV_ERR_NOT_CONVERGED = -4
+RSV_DIAG_FLY = 1
+RSV_DIAG_VEC = 2
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_int_p = ctypes.POINTER(ctypes.c_int)
+c_u64_p = ctypes.POINTER(ctypes.c_uint64)
+c_ll_p = ctypes.POINTER(ctypes.c_longlong)
+
+
+class KrylovReportC(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int),
+        ("converged", ctypes.c_int),
+        ("residual", ctypes.c_double),
+        ("alpha0", ctypes.c_double),
+        ("norm_in", ctypes.c_double),
+        ("substeps", ctypes.c_int),
+        ("matvecs", ctypes.c_int),
+    ]
+
+
+# name -> (restype, argtypes); exactly the symbols declared in include/rsv.h
+SIGNATURES = {
+    "rsv_version": (ctypes.c_int, []),
+    "rsv_last_error": (ctypes.c_char_p, []),
+    "rsv_device_count": (ctypes.c_int, [c_int_p]),
+    "rsv_create": (ctypes.c_int, [ctypes.c_int, c_double_p, ctypes.c_int, ctypes.c_void_p,
+                                  ctypes.POINTER(ctypes.c_void_p)]),
+    "rsv_destroy": (None, [ctypes.c_void_p]),
+    "rsv_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "rsv_bind_slots": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),
+    "rsv_state_slot": (ctypes.c_int, [ctypes.c_void_p, c_int_p]),
+    "rsv_bind_diag_vector": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "rsv_build_diagonal": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_void_p]),
+    "rsv_state_modified": (ctypes.c_int, [ctypes.c_void_p]),
+    "rsv_apply_hamiltonian": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, ctypes.c_void_p,
+                                             ctypes.c_void_p]),
+    "rsv_expm_step": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_int, ctypes.c_double, c_double_p, c_double_p, ctypes.c_int,
+                                     ctypes.POINTER(KrylovReportC)]),
+    "rsv_set_observables": (ctypes.c_int, [ctypes.c_void_p, c_u64_p, ctypes.c_int]),
+    "rsv_get_observables": (ctypes.c_int, [ctypes.c_void_p, c_double_p]),
+    "rsv_measure": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p]),
+    "rsv_observe": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, c_u64_p, ctypes.c_int, c_double_p,
+                                   c_double_p]),
+    "rsv_diff_norm_sq": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                        c_double_p]),
+    "rsv_zdotc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, c_double_p]),
+    "rsv_lanczos_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_uint64, c_double_p]),
+    "rsv_axpy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                ctypes.c_double, ctypes.c_uint64]),
+    "rsv_scale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_uint64]),
+    "rsv_pass_plan": (ctypes.c_int, [ctypes.c_void_p, c_int_p, ctypes.c_int]),
+    "rsv_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rsv_get_profile": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_ll_p]),
+    "rsv_reset_profile": (ctypes.c_int, [ctypes.c_void_p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeError(RydsimError):
+    """The CUDA extension reported an error (or is missing)."""
+
+
+def load():
+    """Load ``_rsv.so`` once; raise NativeError if it is missing (no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(
+                f"CUDA extension {LIB_PATH} is missing; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str = ""):
+    if rc == RSV_OK:
+        return
+    msg = load().rsv_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == RSV_ERR_ARG:
+        raise ValidationError(text)
+    if rc == RSV_ERR_NOT_CONVERGED:
+        raise SolverError(text)
+    raise NativeError(text)
+
+
+def dptr(arr):
+    """ctypes double* for a contiguous float64 numpy array."""
+    return arr.ctypes.data_as(c_double_p)

@@ -1,0 +1,836 @@
+// rsv_capi.cu -- C ABI (include/rsv.h) and the host-side Lanczos step driver.
+//
+// The driver restates rydsim/krylov.py:67-125 (expm_multiply) around the fused
+// pass kernels: per Lanczos iteration it launches the bit-group passes (the last
+// one writes w_j and reduces beta_j and q_{j+1}), copies (alpha_j, beta_j) to
+// pinned host memory, and runs the reference's a-posteriori convergence test on
+// the host with a tridiagonal implicit-QL eigen-solver (k <= 96).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rsv.h"
+#include "rsv_kernels.cuh"
+
+using rsv::cplx;
+typedef std::complex<double> zc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(RSV_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
+
+constexpr double kNsToUs = 1e-3;          // krylov.py:21
+constexpr double kBreakdownRtol = 1e-14;  // krylov.py:25
+constexpr int kScratchJ = 127;            // alpha-partial slot used by plain H.psi
+constexpr int kPartStride = 2 + rsv::kMaxMasks;   // widest partial row (combine)
+
+// ---------------------------------------------------------------- tridiagonal eigen (implicit QL)
+// Eigen-decomposition of the symmetric tridiagonal (d, e); rotations are
+// accumulated only into the requested rows of the eigenvector matrix.
+void tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<std::vector<double>>& rows,
+                const std::vector<int>& row_ids) {
+  const int n = (int)d.size();
+  e.push_back(0.0);
+  const int r = (int)row_ids.size();
+  rows.assign(r, std::vector<double>(n, 0.0));
+  for (int q = 0; q < r; ++q) rows[q][row_ids[q]] = 1.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0;
+    int m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= 1e-300 + 2.2e-16 * dd * 0.5) break;
+      }
+      if (m != l) {
+        if (++iter > 60) break;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double rr = std::hypot(g, 1.0);
+        g = d[m] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(rr) : -std::fabs(rr)));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = m - 1; i >= l; --i) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          rr = std::hypot(f, g);
+          e[i + 1] = rr;
+          if (rr == 0.0) {
+            d[i + 1] -= p;
+            e[m] = 0.0;
+            break;
+          }
+          s = f / rr;
+          c = g / rr;
+          g = d[i + 1] - p;
+          rr = (d[i] - g) * s + 2.0 * c * b;
+          p = s * rr;
+          d[i + 1] = g + p;
+          g = c * rr - b;
+          for (int q = 0; q < r; ++q) {
+            f = rows[q][i + 1];
+            rows[q][i + 1] = s * rows[q][i] + c * f;
+            rows[q][i] = c * rows[q][i] - s * f;
+          }
+        }
+        if (rr == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+}
+
+// exp(-i tau T) e1 (krylov.py:54). With full=false only the last component is exact
+// (all that the convergence test needs); full=true returns every component.
+std::vector<zc> tridiag_exp_e1(const std::vector<double>& a, const std::vector<double>& b, double tau,
+                               bool full) {
+  const int k = (int)a.size();
+  std::vector<zc> y(k, zc(0.0, 0.0));
+  if (k == 1) {
+    y[0] = std::exp(zc(0.0, -tau * a[0]));
+    return y;
+  }
+  std::vector<double> d(a);
+  std::vector<double> e(b.begin(), b.begin() + (k - 1));
+  std::vector<int> ids;
+  if (full) {
+    for (int i = 0; i < k; ++i) ids.push_back(i);
+  } else {
+    ids.push_back(0);
+    ids.push_back(k - 1);
+  }
+  std::vector<std::vector<double>> rows;
+  tridiag_ql(d, e, rows, ids);
+  const std::vector<double>& z0 = rows[0];
+  std::vector<zc> ph(k);
+  for (int m = 0; m < k; ++m) ph[m] = std::exp(zc(0.0, -tau * d[m])) * z0[m];
+  for (size_t q = 0; q < ids.size(); ++q) {
+    zc acc(0.0, 0.0);
+    for (int m = 0; m < k; ++m) acc += rows[q][m] * ph[m];
+    y[ids[q]] = acc;
+  }
+  return y;
+}
+
+struct PassPlan {
+  rsv::Shape sh;
+  int q0;     // first qubit of the group
+  int nq;     // qubits in the group
+  bool lo;    // lo tile (bits [0, a)) carries the diagonal
+};
+
+}  // namespace
+
+struct rsv_context {
+  int n = 0;
+  int diag_mode = RSV_DIAG_FLY;
+  cudaStream_t st = nullptr;
+  int device = 0;
+  double* d_u = nullptr;
+  double* d_sc = nullptr;
+  double* d_part = nullptr;
+  unsigned* d_counter = nullptr;
+  double* d_dl = nullptr;
+  double* d_dvec = nullptr;
+  double* h_pin = nullptr;
+  std::vector<void*> phys;        // bound slots
+  std::vector<int> logical;       // logical slot -> physical; logical 0..K = Krylov s_j, K+1 = work
+  std::vector<PassPlan> plan;
+  std::vector<double> h_u;
+  // caches
+  bool prep_valid = false;
+  std::vector<double> prep_key;
+  bool dl_valid = false;
+  std::vector<double> dl_key;
+  std::vector<uint64_t> masks;
+  cudaEvent_t obs_event = nullptr;
+  bool obs_pending = false;
+  int obs_count = 0;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_pending;   // (event index start, family)
+  int ev_next = 0;
+  double prof_ms[4] = {0, 0, 0, 0};
+  long long prof_n[4] = {0, 0, 0, 0};
+};
+
+namespace {
+
+int kcap(const rsv_context* c) { return (int)c->logical.size() - 2; }
+cplx* slot(const rsv_context* c, int logical_index) {
+  return reinterpret_cast<cplx*>(c->phys[c->logical[logical_index]]);
+}
+cplx* work(const rsv_context* c) { return slot(c, (int)c->logical.size() - 1); }
+
+void build_plan(rsv_context* c) {
+  const int n = c->n;
+  c->plan.clear();
+  const int alo = std::min(n, rsv::kLoBits);
+  PassPlan lo;
+  lo.sh = rsv::Shape{n, alo, alo, 0, 1ull << (n - alo)};
+  lo.q0 = 0;
+  lo.nq = alo;
+  lo.lo = true;
+  c->plan.push_back(lo);
+  const int rem = n - alo;
+  if (rem <= 0) return;
+  const int gmax = 10;   // hi tile = 2^(12-g) contiguous x 2^g strided, runs >= 64 B
+  const int ng = (rem + gmax - 1) / gmax;
+  std::vector<int> sizes;
+  for (int i = 0; i < ng; ++i) sizes.push_back(rem / ng + (i < rem % ng ? 1 : 0));   // descending
+  int top = n;
+  for (int s : sizes) {
+    PassPlan p;
+    const int a = rsv::kLoBits - s;
+    p.sh = rsv::Shape{n, a, top - s, s, 1ull << (n - a - s)};
+    p.q0 = top - s;
+    p.nq = s;
+    p.lo = false;
+    c->plan.push_back(p);
+    top -= s;
+  }
+}
+
+rsv::FlipSet flips_for(const PassPlan& p, const double* omegas) {
+  rsv::FlipSet f{};
+  f.count = 0;
+  for (int q = p.q0; q < p.q0 + p.nq; ++q) {
+    const double cq = 0.5 * omegas[q];
+    if (cq == 0.0) continue;   // zero drives are skipped, as in _kernels.py:19
+    const int local = p.lo ? q : p.sh.a + (q - p.sh.p);
+    f.mask[f.count] = 1 << local;
+    f.coef[f.count] = cq;
+    ++f.count;
+  }
+  return f;
+}
+
+rsv::DiagArgs diag_for(const rsv_context* c, const PassPlan& p, const double* deltas) {
+  rsv::DiagArgs d{};
+  d.mode = rsv::DIAG_NONE;
+  if (!p.lo) return d;
+  d.mode = c->diag_mode == RSV_DIAG_VEC ? rsv::DIAG_VEC : rsv::DIAG_FLY;
+  d.dl = c->d_dl;
+  d.umat = c->d_u;
+  d.dvec = c->d_dvec;
+  for (int i = 0; i < c->n; ++i) d.delta[i] = deltas[i];
+  return d;
+}
+
+int ensure_dl(rsv_context* c, const double* deltas) {
+  const int alo = c->plan[0].sh.a;
+  std::vector<double> key(deltas, deltas + alo);
+  if (c->dl_valid && key == c->dl_key) return RSV_OK;
+  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, nullptr, deltas, c->diag_mode == RSV_DIAG_FLY ? 1 : 0,
+                                c->d_dl, c->st));
+  c->dl_key = key;
+  c->dl_valid = true;
+  return RSV_OK;
+}
+
+// Key of everything the prepared q_0 depends on: last-pass drives (+ detunings if it holds the diagonal).
+std::vector<double> prep_key_for(const rsv_context* c, const double* omegas, const double* deltas) {
+  const PassPlan& last = c->plan.back();
+  std::vector<double> k(omegas + last.q0, omegas + last.q0 + last.nq);
+  if (last.lo) k.insert(k.end(), deltas, deltas + c->n);
+  return k;
+}
+
+void prof_begin(rsv_context* c, int family) {
+  if (!c->prof) return;
+  if (c->ev_next + 2 > (int)c->ev_pool.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->ev_pool.push_back(e);
+    }
+  }
+  cudaEventRecord(c->ev_pool[c->ev_next], c->st);
+  c->ev_pending.push_back({c->ev_next, family});
+  c->ev_next += 2;
+}
+void prof_end(rsv_context* c) {
+  if (!c->prof) return;
+  cudaEventRecord(c->ev_pool[c->ev_pending.back().first + 1], c->st);
+}
+void prof_collect(rsv_context* c) {   // call after a stream sync
+  if (!c->prof) return;
+  for (auto& pe : c->ev_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_pool[pe.first], c->ev_pool[pe.first + 1]);
+    c->prof_ms[pe.second] += ms;
+    c->prof_n[pe.second] += 1;
+  }
+  c->ev_pending.clear();
+  c->ev_next = 0;
+}
+
+int family_of(size_t pass_index, size_t npass) {
+  if (pass_index + 1 == npass) return 2;
+  return pass_index == 0 ? 0 : 1;
+}
+
+// Krylov combination (also "prepare": k = 1, coefficient 1, in place).
+int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, const double* q_omegas,
+                const double* q_deltas, int observe) {
+  rsv::CombineArgs A{};
+  const PassPlan& last = c->plan.back();
+  A.sh = last.sh;
+  A.qsweep = q_omegas != nullptr ? 1 : 0;
+  if (A.qsweep) {
+    A.fl = flips_for(last, q_omegas);
+    A.dg = diag_for(c, last, q_deltas);
+    if (last.lo) {
+      int rc = ensure_dl(c, q_deltas);
+      if (rc) return rc;
+    }
+  } else {
+    A.fl.count = 0;
+    A.dg.mode = rsv::DIAG_NONE;
+  }
+  if (k > rsv::kMaxKrylov) return fail(RSV_ERR_ARG, "Krylov combination of %d vectors exceeds %d", k, rsv::kMaxKrylov);
+  A.k = k;
+  for (int i = 0; i < k; ++i) {
+    A.v[i] = slot(c, i);
+    A.coef[i] = make_double2(coef[i].real(), coef[i].imag());
+  }
+  A.out = out;
+  A.nmask = observe ? (int)c->masks.size() : 0;
+  for (int m = 0; m < A.nmask; ++m) A.mask[m] = c->masks[m];
+  A.sc = c->d_sc;
+  A.part = c->d_part;
+  A.counter = c->d_counter;
+  prof_begin(c, 3);
+  CUDA_TRY(rsv::launch_combine(A, rsv::pass_grid(A.sh), c->st));
+  prof_end(c);
+  if (A.nmask > 0) {
+    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_OBS, c->d_sc + rsv::SC_OBS, sizeof(double) * A.nmask,
+                             cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_N0SQ, c->d_sc + rsv::SC_N0SQ, sizeof(double),
+                             cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaEventRecord(c->obs_event, c->st));
+    c->obs_pending = true;
+    c->obs_count = A.nmask;
+  }
+  return RSV_OK;
+}
+
+int prepare(rsv_context* c, const double* omegas, const double* deltas) {
+  std::vector<zc> one(1, zc(1.0, 0.0));
+  int rc = run_combine(c, 1, one, slot(c, 0), omegas, deltas, 0);
+  if (rc) return rc;
+  c->prep_key = prep_key_for(c, omegas, deltas);
+  c->prep_valid = true;
+  return RSV_OK;
+}
+
+int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const double* deltas) {
+  const size_t np = c->plan.size();
+  for (size_t pi = 0; pi < np; ++pi) {
+    const PassPlan& p = c->plan[pi];
+    rsv::PassArgs A{};
+    A.sh = p.sh;
+    A.fl = flips_for(p, omegas);
+    A.dg = diag_for(c, p, deltas);
+    A.x = slot(c, j);
+    A.x_scale_slot = rsv::SC_SG + j;
+    A.j = j;
+    A.sc = c->d_sc;
+    A.part = c->d_part;
+    A.counter = c->d_counter;
+    const bool last = pi + 1 == np;
+    if (!last) {
+      A.kind = pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID;
+      A.uin = pi == 0 ? nullptr : work(c);
+      A.out = work(c);
+    } else {
+      A.kind = rsv::PASS_LAST_LANCZOS;
+      A.uin = np > 1 ? work(c) : nullptr;
+      A.out = slot(c, j + 1);
+      A.prev = j > 0 ? slot(c, j - 1) : nullptr;
+      A.qsweep = 1;
+    }
+    prof_begin(c, family_of(pi, np));
+    CUDA_TRY(rsv::launch_pass(A, rsv::pass_grid(A.sh), c->st));
+    prof_end(c);
+  }
+  return RSV_OK;
+}
+
+// One exact step of length dt on the resident state (may recurse into sub-steps).
+int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, double dt_ns, double tol,
+                   int kmax, double norm_eps, const double* next_omegas, const double* next_deltas,
+                   int observe, rsv_krylov_report* rep, int depth) {
+  if (depth > 24) return fail(RSV_ERR_NOT_CONVERGED, "sub-step recursion too deep");
+  if (!c->prep_valid || c->prep_key != prep_key_for(c, omegas, deltas)) {
+    int rc = prepare(c, omegas, deltas);
+    if (rc) return rc;
+  }
+  int rc = ensure_dl(c, deltas);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemsetAsync(c->d_sc + rsv::SC_AP, 0, sizeof(double) * 128, c->st));
+
+  const double tau = dt_ns * kNsToUs;
+  const int cap = kcap(c);
+  std::vector<double> alphas, betas;
+  std::vector<zc> y;
+  double residual = INFINITY, n0 = 0.0, beta = 0.0;
+  bool converged = false;
+  int k = 0;
+  for (int j = 0;; ++j) {
+    rc = launch_lanczos_iteration(c, j, omegas, deltas);
+    if (rc) return rc;
+    rep->matvecs += 1;
+    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_AL + j, c->d_sc + rsv::SC_AL + j, sizeof(double),
+                             cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_BE + j, c->d_sc + rsv::SC_BE + j, sizeof(double),
+                             cudaMemcpyDeviceToHost, c->st));
+    if (j == 0)
+      CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_N0SQ, c->d_sc + rsv::SC_N0SQ, sizeof(double),
+                               cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    prof_collect(c);
+    if (j == 0) {
+      n0 = std::sqrt(std::max(0.0, c->h_pin[rsv::SC_N0SQ]));
+      rep->norm_in = n0;
+      if (n0 <= norm_eps) {   // krylov.py:83-84: zero vector returned unchanged
+        rep->iterations = std::max(rep->iterations, 0);
+        rep->converged = 1;
+        rep->residual = 0.0;
+        return RSV_OK;
+      }
+      rep->alpha0 = c->h_pin[rsv::SC_AL];
+    }
+    alphas.push_back(c->h_pin[rsv::SC_AL + j]);
+    beta = c->h_pin[rsv::SC_BE + j];
+    y = tridiag_exp_e1(alphas, betas, tau, false);
+    residual = beta * std::abs(y.back());
+    k = (int)alphas.size();
+    double scale = 1.0;
+    for (double a : alphas) scale = std::max(scale, std::fabs(a));
+    for (double b : betas) scale = std::max(scale, b);
+    if (residual <= tol || beta <= kBreakdownRtol * scale) {   // krylov.py:111
+      converged = true;
+      break;
+    }
+    if (k >= kmax) break;                                       // krylov.py:114
+    if (k >= cap) break;                                        // HBM cap: split below
+    betas.push_back(beta);
+  }
+
+  double tau_used = tau;
+  int nsub = 1;
+  if (!converged && k >= cap && k < kmax) {
+    // Split exp(-i tau H) = exp(-i tau/2^s H)^(2^s): the same Krylov basis gives the
+    // first sub-step; the rest are fresh Lanczos runs on the advanced state.
+    for (int s = 1; s <= 20; ++s) {
+      const double ts = tau / double(1 << s);
+      std::vector<zc> ys = tridiag_exp_e1(alphas, betas, ts, false);
+      if (beta * std::abs(ys.back()) <= tol) {
+        tau_used = ts;
+        nsub = 1 << s;
+        residual = beta * std::abs(ys.back());
+        converged = true;
+        break;
+      }
+    }
+  }
+  y = tridiag_exp_e1(alphas, betas, tau_used, true);
+  rep->iterations = std::max(rep->iterations, k);
+  rep->residual = std::max(depth == 0 ? 0.0 : rep->residual, residual);
+  rep->converged = (depth == 0 ? 1 : rep->converged) && converged;
+
+  // psi_new = n0 * sum_i y_i v_i, v_0 = s_0/n0, v_i = s_i / beta_{i-1}
+  std::vector<zc> coef(k);
+  for (int i = 0; i < k; ++i) {
+    const double sigma = i == 0 ? 1.0 / n0 : 1.0 / betas[i - 1];
+    coef[i] = y[i] * (n0 * sigma);
+  }
+  const bool more = nsub > 1;
+  const double* qo = more ? omegas : next_omegas;
+  const double* qd = more ? deltas : next_deltas;
+  rc = run_combine(c, k, coef, work(c), qo, qd, (!more && observe) ? 1 : 0);
+  if (rc) return rc;
+  std::swap(c->logical[0], c->logical[c->logical.size() - 1]);
+  if (qo != nullptr) {
+    c->prep_key = prep_key_for(c, qo, qd);
+    c->prep_valid = true;
+  } else {
+    c->prep_valid = false;
+  }
+  if (more) {
+    rep->substeps += nsub - 1;
+    const double dts = dt_ns / nsub;
+    for (int r = 1; r < nsub; ++r) {
+      const bool final_sub = r + 1 == nsub;
+      rc = expm_step_impl(c, omegas, deltas, dts, tol, kmax, norm_eps, final_sub ? next_omegas : omegas,
+                          final_sub ? next_deltas : deltas, final_sub ? observe : 0, rep, depth + 1);
+      if (rc) return rc;
+    }
+  }
+  return RSV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsv_version(void) { return 10000; }
+
+const char* rsv_last_error(void) { return g_err.c_str(); }
+
+int rsv_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return fail(RSV_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *out = n;
+  return RSV_OK;
+}
+
+int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* stream, rsv_context** out) {
+  if (out == nullptr) return fail(RSV_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > rsv::kMaxQubits)
+    return fail(RSV_ERR_ARG, "n_qubits=%d outside [1, %d]", n_qubits, rsv::kMaxQubits);
+  if (diag_mode != RSV_DIAG_FLY && diag_mode != RSV_DIAG_VEC)
+    return fail(RSV_ERR_ARG, "unknown diag_mode %d", diag_mode);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(RSV_ERR_CUDA, "no CUDA device: the rsv hot path has no CPU fallback");
+  rsv_context* c = new rsv_context();
+  c->n = n_qubits;
+  c->diag_mode = diag_mode;
+  c->st = reinterpret_cast<cudaStream_t>(stream);
+  cudaGetDevice(&c->device);
+  c->h_u.assign(interaction_u, interaction_u + (size_t)n_qubits * n_qubits);
+  build_plan(c);
+  int maxgrid = rsv::max_pass_grid(rsv::kLoBits) * 2;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_u, sizeof(double) * n_qubits * n_qubits);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sc, sizeof(double) * rsv::SC_SIZE);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_part, sizeof(double) * (size_t)maxgrid * kPartStride);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl, sizeof(double) << rsv::kLoBits);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_pin, sizeof(double) * rsv::SC_SIZE);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->obs_event, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->d_u, c->h_u.data(), sizeof(double) * n_qubits * n_qubits, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(c->d_counter, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMemset(c->d_sc, 0, sizeof(double) * rsv::SC_SIZE);
+  double one = 1.0;
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_sc + rsv::SC_ONE, &one, sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    rsv_destroy(c);
+    return fail(RSV_ERR_CUDA, "rsv_create: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return RSV_OK;
+}
+
+void rsv_destroy(rsv_context* c) {
+  if (c == nullptr) return;
+  cudaFree(c->d_u);
+  cudaFree(c->d_sc);
+  cudaFree(c->d_part);
+  cudaFree(c->d_counter);
+  cudaFree(c->d_dl);
+  if (c->h_pin) cudaFreeHost(c->h_pin);
+  if (c->obs_event) cudaEventDestroy(c->obs_event);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+int rsv_set_stream(rsv_context* c, void* stream) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  c->st = reinterpret_cast<cudaStream_t>(stream);
+  return RSV_OK;
+}
+
+int rsv_bind_slots(rsv_context* c, void* const* slots, int nslots) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (nslots < 3) return fail(RSV_ERR_ARG, "need at least 3 slots (2 Krylov vectors + work), got %d", nslots);
+  if (nslots - 2 > rsv::kMaxKrylov)
+    nslots = rsv::kMaxKrylov + 2;   // extra slots are never used
+  c->phys.assign(slots, slots + nslots);
+  for (int i = 0; i < nslots; ++i) {
+    if (c->phys[i] == nullptr || (reinterpret_cast<uintptr_t>(c->phys[i]) & 15u))
+      return fail(RSV_ERR_ARG, "slot %d is NULL or not 16-byte aligned", i);
+  }
+  c->logical.resize(nslots);
+  for (int i = 0; i < nslots; ++i) c->logical[i] = i;
+  c->prep_valid = false;
+  return RSV_OK;
+}
+
+int rsv_state_slot(rsv_context* c, int* out) {
+  if (!c || c->logical.empty()) return fail(RSV_ERR_STATE, "no slots bound");
+  *out = c->logical[0];
+  return RSV_OK;
+}
+
+int rsv_bind_diag_vector(rsv_context* c, double* dev_diag, int fill_interaction) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  c->d_dvec = dev_diag;
+  if (dev_diag != nullptr && fill_interaction) {
+    CUDA_TRY(rsv::launch_interaction_diag(c->n, c->d_u, nullptr, dev_diag, c->st));
+  }
+  c->prep_valid = false;
+  return RSV_OK;
+}
+
+int rsv_build_diagonal(rsv_context* c, const double* deltas, double* dev_out) {
+  if (!c || !deltas || !dev_out) return fail(RSV_ERR_ARG, "NULL argument");
+  CUDA_TRY(rsv::launch_interaction_diag(c->n, c->d_u, deltas, dev_out, c->st));
+  return RSV_OK;
+}
+
+int rsv_state_modified(rsv_context* c) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  c->prep_valid = false;
+  return RSV_OK;
+}
+
+int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* deltas, const void* psi, void* out) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (psi == nullptr || out == nullptr) return fail(RSV_ERR_ARG, "NULL vector");
+  if (c->diag_mode == RSV_DIAG_VEC && c->d_dvec == nullptr)
+    return fail(RSV_ERR_STATE, "diag_mode VEC needs rsv_bind_diag_vector first");
+  const size_t np = c->plan.size();
+  if (np > 1 && psi == out) return fail(RSV_ERR_ARG, "psi and out must not alias for N > %d", rsv::kLoBits);
+  int rc = ensure_dl(c, deltas);
+  if (rc) return rc;
+  for (size_t pi = 0; pi < np; ++pi) {
+    const PassPlan& p = c->plan[pi];
+    rsv::PassArgs A{};
+    A.sh = p.sh;
+    A.fl = flips_for(p, omegas);
+    A.dg = diag_for(c, p, deltas);
+    A.x = reinterpret_cast<const cplx*>(psi);
+    A.x_scale_slot = rsv::SC_ONE;
+    A.j = kScratchJ;
+    A.sc = c->d_sc;
+    A.part = c->d_part;
+    A.counter = c->d_counter;
+    A.out = reinterpret_cast<cplx*>(out);
+    if (pi + 1 == np) {
+      A.kind = rsv::PASS_LAST_APPLY;
+      A.uin = np > 1 ? reinterpret_cast<const cplx*>(out) : nullptr;
+    } else {
+      A.kind = pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID;
+      A.uin = pi == 0 ? nullptr : reinterpret_cast<const cplx*>(out);
+    }
+    prof_begin(c, family_of(pi, np));
+    CUDA_TRY(rsv::launch_pass(A, rsv::pass_grid(A.sh), c->st));
+    prof_end(c);
+  }
+  return RSV_OK;
+}
+
+int rsv_expm_step(rsv_context* c, const double* omegas, const double* deltas, double dt_ns, double tolerance,
+                  int max_krylov_dim, double norm_epsilon, const double* next_omegas, const double* next_deltas,
+                  int observe, rsv_krylov_report* report) {
+  if (!c || !report || !omegas || !deltas) return fail(RSV_ERR_ARG, "NULL argument");
+  if (c->logical.empty()) return fail(RSV_ERR_STATE, "no slots bound");
+  if (c->diag_mode == RSV_DIAG_VEC && c->d_dvec == nullptr)
+    return fail(RSV_ERR_STATE, "diag_mode VEC needs rsv_bind_diag_vector first");
+  if (max_krylov_dim < 2) return fail(RSV_ERR_ARG, "max_krylov_dim must be >= 2");
+  if (max_krylov_dim > rsv::kMaxKrylov) max_krylov_dim = rsv::kMaxKrylov;
+  std::memset(report, 0, sizeof(*report));
+  if (dt_ns == 0.0) {   // krylov.py:85-86: identity, one iteration
+    report->iterations = 1;
+    report->converged = 1;
+    if (observe) {
+      double nsq = 0.0;
+      std::vector<double> tmp(c->masks.size());
+      int rc = rsv_measure(c, tmp.data(), &nsq);
+      if (rc) return rc;
+      report->norm_in = std::sqrt(nsq);
+    }
+    return RSV_OK;
+  }
+  return expm_step_impl(c, omegas, deltas, dt_ns, tolerance, max_krylov_dim, norm_epsilon, next_omegas,
+                        next_deltas, observe, report, 0);
+}
+
+int rsv_set_observables(rsv_context* c, const uint64_t* masks, int nmask) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (nmask < 0 || nmask > rsv::kMaxMasks) return fail(RSV_ERR_ARG, "nmask %d outside [0, %d]", nmask, rsv::kMaxMasks);
+  c->masks.assign(masks, masks + nmask);
+  return RSV_OK;
+}
+
+int rsv_get_observables(rsv_context* c, double* out) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (!c->obs_pending) return fail(RSV_ERR_STATE, "no observables were requested on the last step");
+  CUDA_TRY(cudaEventSynchronize(c->obs_event));
+  const double nsq = c->h_pin[rsv::SC_N0SQ];
+  for (int m = 0; m < c->obs_count; ++m) out[m] = nsq > 0.0 ? c->h_pin[rsv::SC_OBS + m] / nsq : 0.0;
+  return RSV_OK;
+}
+
+int rsv_measure(rsv_context* c, double* out, double* norm_sq) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (c->logical.empty()) return fail(RSV_ERR_STATE, "no slots bound");
+  std::vector<zc> one(1, zc(1.0, 0.0));
+  int rc = run_combine(c, 1, one, slot(c, 0), nullptr, nullptr, 1);
+  if (rc) return rc;
+  c->prep_valid = false;
+  if (!c->obs_pending) {   // no masks: still report the norm
+    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_N0SQ, c->d_sc + rsv::SC_N0SQ, sizeof(double),
+                             cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    prof_collect(c);
+    if (norm_sq) *norm_sq = c->h_pin[rsv::SC_N0SQ];
+    return RSV_OK;
+  }
+  rc = rsv_get_observables(c, out);
+  prof_collect(c);
+  if (norm_sq) *norm_sq = c->h_pin[rsv::SC_N0SQ];
+  return rc;
+}
+
+int rsv_observe(rsv_context* c, const void* psi, const uint64_t* masks, int nmask, double* out, double* norm_sq) {
+  if (!c || !psi) return fail(RSV_ERR_ARG, "NULL argument");
+  if (nmask < 0 || nmask > rsv::kMaxMasks) return fail(RSV_ERR_ARG, "nmask %d outside [0, %d]", nmask, rsv::kMaxMasks);
+  rsv::CombineArgs A{};
+  A.sh = c->plan.back().sh;
+  A.fl.count = 0;
+  A.dg.mode = rsv::DIAG_NONE;
+  A.k = 1;
+  A.v[0] = reinterpret_cast<const cplx*>(psi);
+  A.coef[0] = make_double2(1.0, 0.0);
+  A.out = nullptr;   // read-only
+  A.qsweep = 0;
+  A.nmask = nmask;
+  for (int m = 0; m < nmask; ++m) A.mask[m] = masks[m];
+  A.sc = c->d_sc;
+  A.part = c->d_part;
+  A.counter = c->d_counter;
+  // the combine overwrites SC_N0SQ / SC_SG / SC_Q: the resident state is re-prepared on its next step
+  CUDA_TRY(rsv::launch_combine(A, rsv::pass_grid(A.sh), c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_OBS, c->d_sc + rsv::SC_OBS, sizeof(double) * (nmask > 0 ? nmask : 1),
+                           cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_SIZE - 3, c->d_sc + rsv::SC_N0SQ, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->prep_valid = false;
+  const double nsq = c->h_pin[rsv::SC_SIZE - 3];
+  for (int m = 0; m < nmask; ++m) out[m] = nsq > 0.0 ? c->h_pin[rsv::SC_OBS + m] / nsq : 0.0;
+  if (norm_sq) *norm_sq = nsq;
+  return RSV_OK;
+}
+
+int rsv_diff_norm_sq(rsv_context* c, const void* x, const void* y, uint64_t n, double* out) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  CUDA_TRY(rsv::launch_diff_norm(reinterpret_cast<const cplx*>(x), reinterpret_cast<const cplx*>(y), n, c->d_part,
+                                 c->d_counter, c->d_sc + rsv::SC_OBS, 0, c->st));
+  CUDA_TRY(cudaMemcpyAsync(out, c->d_sc + rsv::SC_OBS, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return RSV_OK;
+}
+
+int rsv_zdotc(rsv_context* c, const void* x, const void* y, uint64_t n, double* out) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  CUDA_TRY(rsv::launch_zdotc(reinterpret_cast<const cplx*>(x), reinterpret_cast<const cplx*>(y), n, c->d_part,
+                             c->d_counter, c->d_sc + rsv::SC_OBS, 0, c->st));
+  CUDA_TRY(cudaMemcpyAsync(out, c->d_sc + rsv::SC_OBS, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return RSV_OK;
+}
+
+int rsv_lanczos_update(rsv_context* c, void* w, const void* v, const void* vprev, double alpha, double beta,
+                       uint64_t n, double* out_norm_sq) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  CUDA_TRY(rsv::launch_lanczos_update(reinterpret_cast<cplx*>(w), reinterpret_cast<const cplx*>(v),
+                                      reinterpret_cast<const cplx*>(vprev), alpha, beta, n, c->d_part,
+                                      c->d_counter, c->d_sc + rsv::SC_OBS, 0, c->st));
+  CUDA_TRY(cudaMemcpyAsync(out_norm_sq, c->d_sc + rsv::SC_OBS, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return RSV_OK;
+}
+
+int rsv_axpy(rsv_context* c, void* y, const void* x, double are, double aim, uint64_t n) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  CUDA_TRY(rsv::launch_axpy(reinterpret_cast<cplx*>(y), reinterpret_cast<const cplx*>(x), make_double2(are, aim),
+                            n, 0, c->st));
+  return RSV_OK;
+}
+
+int rsv_scale(rsv_context* c, void* y, const void* x, double are, double aim, uint64_t n) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  CUDA_TRY(rsv::launch_scale(reinterpret_cast<cplx*>(y), reinterpret_cast<const cplx*>(x), make_double2(are, aim),
+                             n, 0, c->st));
+  return RSV_OK;
+}
+
+int rsv_pass_plan(rsv_context* c, int* out, int max_ints) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  const int np = (int)c->plan.size();
+  if (max_ints < 1 + 5 * np) return fail(RSV_ERR_ARG, "buffer too small");
+  out[0] = np;
+  for (int i = 0; i < np; ++i) {
+    out[1 + 5 * i] = c->plan[i].sh.a;
+    out[2 + 5 * i] = c->plan[i].sh.p;
+    out[3 + 5 * i] = c->plan[i].sh.g;
+    out[4 + 5 * i] = c->plan[i].lo ? 1 : 0;
+    out[5 + 5 * i] = family_of(i, np);
+  }
+  return RSV_OK;
+}
+
+int rsv_set_profiling(rsv_context* c, int on) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  c->prof = on != 0;
+  return RSV_OK;
+}
+
+int rsv_get_profile(rsv_context* c, double* ms4, long long* n4) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  for (int i = 0; i < 4; ++i) {
+    ms4[i] = c->prof_ms[i];
+    n4[i] = c->prof_n[i];
+  }
+  return RSV_OK;
+}
+
+int rsv_reset_profile(rsv_context* c) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  for (int i = 0; i < 4; ++i) {
+    c->prof_ms[i] = 0;
+    c->prof_n[i] = 0;
+  }
+  return RSV_OK;
+}
+
+}  // extern "C"

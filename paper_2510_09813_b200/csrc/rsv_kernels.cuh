@@ -1,0 +1,131 @@
+// rsv_kernels.cuh -- sm_100a kernels for the matrix-free Rydberg H.psi and the fused Lanczos step.
+//
+// State layout in HBM: one complex128 (double2, 16 B) per basis index b in [0, 2^N);
+// qubit i is bit i of b (reference convention, rydsim/hamiltonian.py:1-8).
+//
+// H.psi (rydsim/hamiltonian.py:164 apply_hamiltonian, rydsim/_kernels.py:14) is
+//   out[b] = d[b] psi[b] + sum_i (Omega_i/2) psi[b ^ (1<<i)]
+// Every bit flip must see both partners on chip, but one CTA can hold only 2^12
+// amplitudes (64 KB of shared memory), so the N qubits are partitioned into
+// "bit groups", one streaming pass each:
+//   * the lo pass: tile = bits [0, a) contiguous (a = min(N, 12)); applies the
+//     flips on those bits plus the diagonal (on the fly from U, or from a
+//     precomputed vector);
+//   * hi passes: tile = 2^a contiguous amplitudes (64..512 B runs, full DRAM
+//     bursts) x 2^g amplitudes strided along a group of g high bits; applies
+//     the flips on the group.
+// A tile is loaded once with cp.async into shared memory; each partner of a
+// flip is then one 16-byte shared load (bank-conflict free: e ^ mask permutes
+// aligned groups of 8 lanes).
+//
+// The Lanczos recurrence is fused into the passes (no separate vdot/axpy/norm
+// passes): the first/middle passes reduce their part of alpha_j = <v_j|H|v_j>,
+// the last pass knows alpha_j completely (its own part q_j was computed one
+// iteration earlier from w_{j-1} while that tile was on chip, the "q-sweep"),
+// so it writes w_j = H v_j - alpha_j v_j - beta_{j-1} v_{j-1} directly and
+// reduces ||w_j||^2 and q_{j+1}. Vectors are kept unnormalised with scales in a
+// device scalar array, so normalisation costs no pass.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rsv {
+
+typedef double2 cplx;
+
+constexpr int kMaxQubits = 48;
+constexpr int kMaxFlips = 16;     // flips per pass (tile bits <= 12)
+constexpr int kMaxKrylov = 96;    // vectors in one Krylov combination
+constexpr int kMaxMasks = 128;    // observable masks per combine
+constexpr int kLoBits = 12;       // tile bits (2^12 complex128 = 64 KB)
+
+// scalar slots (device double array, reset per step)
+constexpr int SC_N0SQ = 0;        // ||psi||^2 of the step's input state
+constexpr int SC_ONE = 1;         // constant 1.0
+constexpr int SC_AP = 16;         // partial alpha (first+mid passes), per iteration
+constexpr int SC_Q = SC_AP + 128; // q_j = <v_j|A_last|v_j>
+constexpr int SC_AL = SC_Q + 128; // alpha_j
+constexpr int SC_BE = SC_AL + 128;// beta_j
+constexpr int SC_SG = SC_BE + 128;// sigma_j : v_j = sigma_j * s_j
+constexpr int SC_OBS = SC_SG + 128;
+constexpr int SC_SIZE = SC_OBS + kMaxMasks + 8;
+
+enum PassKind : int {
+  PASS_FIRST = 0,         // out = A x            ; ap[j]  = <x|A x>
+  PASS_MID = 1,           // out = uin + A x      ; ap[j] += <x|A x>
+  PASS_LAST_APPLY = 2,    // out = uin + A x       (plain H.psi)
+  PASS_LAST_LANCZOS = 3,  // out = uin + A x - alpha x - beta' prev ; beta, q_{j+1}
+};
+
+enum DiagMode : int { DIAG_NONE = 0, DIAG_FLY = 1, DIAG_VEC = 2 };
+
+struct Shape {
+  int n;        // local qubits
+  int a;        // contiguous low bits in the tile
+  int p;        // first bit of the strided group (p >= a)
+  int g;        // bits in the group
+  uint64_t n_tiles;
+};
+
+struct FlipSet {
+  int count;
+  int mask[kMaxFlips];      // tile-local bit masks
+  double coef[kMaxFlips];   // Omega_q / 2
+};
+
+struct DiagArgs {
+  int mode;                 // DiagMode (only for passes whose tile is [0, a))
+  const double* dl;         // 2^a table: lo part of the diagonal (fly: detuning+interaction, vec: detuning)
+  const double* umat;       // n x n interaction matrix (fly)
+  const double* dvec;       // 2^n precomputed interaction diagonal (vec)
+  double delta[kMaxQubits]; // detunings
+};
+
+struct PassArgs {
+  Shape sh;
+  FlipSet fl;
+  DiagArgs dg;
+  int kind;
+  const cplx* x; int x_scale_slot;      // operand s_j, v_j = sc[slot] * s_j
+  const cplx* uin;                      // partial sum from previous passes (may be null)
+  cplx* out;
+  const cplx* prev;                     // s_{j-1} (LAST_LANCZOS, j > 0)
+  int j;                                // Lanczos iteration
+  int qsweep;                           // LAST_LANCZOS: compute q_{j+1}
+  double* sc; double* part; unsigned* counter;
+};
+
+struct CombineArgs {
+  Shape sh;
+  FlipSet fl;                           // next step's flips on this tile's group (q-sweep)
+  DiagArgs dg;                          // next step's diagonal if the group is the lo tile
+  int k;
+  const cplx* v[kMaxKrylov];
+  double2 coef[kMaxKrylov];             // psi_new = sum coef_i * v_i
+  cplx* out;
+  int qsweep;
+  int nmask;                            // observables: sum_b |psi_b|^2 [b & M == M]
+  uint64_t mask[kMaxMasks];
+  double* sc; double* part; unsigned* counter;
+};
+
+// host-side launchers (rsv_kernels.cu)
+cudaError_t launch_pass(const PassArgs& args, int grid, cudaStream_t st);
+cudaError_t launch_combine(const CombineArgs& args, int grid, cudaStream_t st);
+cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_dev_or_null,
+                            const double* delta_host, int with_interaction, double* dl, cudaStream_t st);
+cudaError_t launch_interaction_diag(int n, const double* umat, const double* delta_host, double* dvec,
+                                    cudaStream_t st);
+cudaError_t launch_zdotc(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter,
+                         double* result2, int grid, cudaStream_t st);
+cudaError_t launch_diff_norm(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter,
+                             double* result, int grid, cudaStream_t st);
+cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, double alpha, double beta,
+                                  uint64_t n, double* part, unsigned* counter, double* result, int grid,
+                                  cudaStream_t st);
+cudaError_t launch_axpy(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
+cudaError_t launch_scale(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
+int max_pass_grid(int tile_bits);
+int pass_grid(const Shape& sh);
+
+}  // namespace rsv

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors and the
+CPU oracle on the same seeded inputs. Tolerances are written per test:
+
+* H.psi: relative 1e-12 of max |H psi| (reference: hamiltonian tests use 1e-12);
+* Lanczos step: ||out - ref|| <= 100 p (krylov.py tests), p = Krylov tolerance;
+* evolution: fidelity 1 - |<ref|gpu>|^2 <= 1e-10 and observables within 1e-8 absolute
+  (north-star acceptance), plus ||out - ref|| <= 1e-8.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import sv_oracle as O
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+@pytest.fixture(scope="module")
+def rs():
+    import paper_2510_09813_b200 as pkg
+
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    return t
+
+
+def random_slice(rng, n):
+    om = rng.uniform(0.0, 4.0, n)
+    de = rng.uniform(-3.0, 3.0, n)
+    u = np.triu(rng.uniform(0.0, 2.0, (n, n)), 1)
+    return om, de, u + u.T
+
+
+def rel_err(a, b):
+    return np.abs(a - b).max() / max(1.0, np.abs(b).max())
+
+
+class TestApplyHamiltonian:
+    def test_golden_vectors(self, rs):
+        g = load("apply_hamiltonian.npz")
+        for n in (1, 2, 3, 4, 5, 7, 8, 10, 11, 12, 13):
+            s = rs.HamiltonianSlice.from_parameters(g[f"n{n}_omegas"], g[f"n{n}_deltas"], g[f"n{n}_u"])
+            out = rs.apply_hamiltonian(s, g[f"n{n}_psi"])
+            assert rel_err(out, g[f"n{n}_hpsi"]) <= 1e-12, n
+
+    def test_explicit_diagonal_vec_mode(self, rs):
+        g = load("apply_hamiltonian.npz")
+        for n in (3, 10, 13):
+            s = rs.HamiltonianSlice(g[f"n{n}_omegas"], g[f"n{n}_diag"])
+            out = rs.apply_hamiltonian(s, g[f"n{n}_psi"])
+            assert rel_err(out, g[f"n{n}_hpsi"]) <= 1e-12, n
+
+    @pytest.mark.parametrize("n", [14, 17, 20, 22, 23, 24])
+    def test_multi_pass_against_oracle(self, rs, torch, n):
+        # 13..22 qubits: lo pass + 1 group pass; >= 23: lo + 2 group passes
+        rng = np.random.default_rng(n)
+        om, de, u = random_slice(rng, n)
+        om[n // 2] = 0.0   # a zero drive is skipped by the kernel
+        psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        ref = O.apply_hamiltonian(om, O.build_diagonal(de, u), psi)
+        s = rs.HamiltonianSlice.from_parameters(om, de, u)
+        out = rs.apply_hamiltonian(s, torch.from_numpy(psi).cuda()).cpu().numpy()
+        assert rel_err(out, ref) <= 1e-12
+
+    def test_build_diagonal_on_device(self, rs):
+        g = load("diagonal.npz")
+        for n in (1, 2, 6, 9):
+            d = rs.build_diagonal(g[f"n{n}_deltas"], g[f"n{n}_u"]).cpu().numpy()
+            assert np.abs(d - g[f"n{n}_diag"]).max() <= 1e-12 * max(1, np.abs(d).max())
+
+    def test_linearity_and_hermiticity_large(self, rs, torch):
+        n = 26
+        rng = np.random.default_rng(3)
+        om, de, u = random_slice(rng, n)
+        s = rs.HamiltonianSlice.from_parameters(om, de, u)
+        gen = torch.Generator(device="cuda").manual_seed(1)
+        x = torch.randn(2 ** n, dtype=torch.complex128, device="cuda", generator=gen)
+        y = torch.randn(2 ** n, dtype=torch.complex128, device="cuda", generator=gen)
+        hx = rs.apply_hamiltonian(s, x)
+        hy = rs.apply_hamiltonian(s, y)
+        # <y|Hx> = conj(<x|Hy>) for Hermitian H (size-independent property)
+        a = rs.overlap(y, hx)
+        b = rs.overlap(x, hy).conjugate()
+        assert abs(a - b) <= 1e-10 * abs(a)
+        e = rs.overlap(x, hx)
+        assert abs(e.imag) <= 1e-10 * abs(e.real)
+
+
+class TestExpm:
+    def test_golden_lanczos_steps(self, rs):
+        g = load("expm_multiply.npz")
+        p = 1e-10
+        for n in range(2, 11):
+            s = rs.HamiltonianSlice.from_parameters(g[f"n{n}_omegas"], g[f"n{n}_deltas"], g[f"n{n}_u"])
+            out, rep = rs.expm_multiply(s, g[f"n{n}_psi"], float(g[f"n{n}_dt"]), rs.KrylovConfig(p))
+            assert rep.converged
+            assert np.linalg.norm(out - g[f"n{n}_out"]) <= 100 * p, n
+            assert abs(rep.iterations - int(g[f"n{n}_iterations"])) <= 1
+
+    def test_generic_callable_path(self, rs, torch):
+        lam = torch.linspace(-5, 5, 64, dtype=torch.float64, device="cuda")
+        rng = np.random.default_rng(0)
+        psi = torch.from_numpy(rng.standard_normal(64) + 1j * rng.standard_normal(64)).cuda()
+        out, rep = rs.expm_multiply(lambda v: lam * v, psi, 150.0, rs.KrylovConfig(1e-12))
+        exp = torch.exp(-1j * lam * 0.150) * psi
+        assert rep.converged and (out - exp).abs().max().item() <= 1e-11
+
+    def test_edge_cases(self, rs):
+        s = rs.HamiltonianSlice.from_parameters([1.0, 2.0], [0.3, -0.2], np.array([[0, 3.0], [3.0, 0]]))
+        psi = np.array([0.5, 0.5j, -0.5, 0.5], dtype=complex)
+        out, rep = rs.expm_multiply(s, psi, 0.0)
+        assert np.array_equal(out, psi) and rep.iterations == 1 and rep.converged
+        out, rep = rs.expm_multiply(s, np.zeros(4, complex), 10.0)
+        assert rep.iterations == 0 and rep.converged and not np.any(out)
+        # eigenvector terminates early: |00> with zero drive
+        s0 = rs.HamiltonianSlice.from_parameters([0.0, 0.0], [0.3, -0.2], np.zeros((2, 2)))
+        out, rep = rs.expm_multiply(s0, np.array([0, 1, 0, 0], complex), 100.0, rs.KrylovConfig(1e-12))
+        assert rep.converged and rep.iterations <= 2
+        assert abs(out[1] - np.exp(1j * 0.3 * 0.1)) <= 1e-12
+
+    def test_forward_backward_large(self, rs, torch):
+        n = 24
+        rng = np.random.default_rng(5)
+        om, de, u = random_slice(rng, n)
+        s = rs.HamiltonianSlice.from_parameters(om, de, u)
+        gen = torch.Generator(device="cuda").manual_seed(2)
+        psi = torch.randn(2 ** n, dtype=torch.complex128, device="cuda", generator=gen)
+        psi /= torch.linalg.vector_norm(psi)
+        fwd, r1 = rs.expm_multiply(s, psi, 5.0, rs.KrylovConfig(1e-12))
+        back, r2 = rs.expm_multiply(s, fwd, -5.0, rs.KrylovConfig(1e-12))
+        assert r1.converged and r2.converged
+        assert abs(rs.norm_difference(fwd, fwd) ) == 0.0
+        assert rs.norm_difference(back, psi) <= 1e-9
+        assert abs(math.sqrt(abs(rs.overlap(fwd, fwd))) - 1.0) <= 1e-10
+
+
+def run_gpu(rs, g, every, pairs=(), energy=False, diag="fly"):
+    n = g["omegas"].shape[1]
+    reg = rs.Register(tuple(map(tuple, g["positions"])), float(g["c6"]))
+    seq = rs.DiscretizedSequence(int(g["dt"]), g["omegas"], g["deltas"], int(g["dt"]) * g["omegas"].shape[0])
+    specs = [rs.ObservableSpec("occupation", (), every)]
+    if len(pairs):
+        specs.append(rs.ObservableSpec("correlation", tuple(int(q) for p in pairs for q in p), 0))
+    if energy:
+        specs.append(rs.ObservableSpec("energy", (), 0))
+    cfg = rs.SvRunConfig(krylov=rs.KrylovConfig(float(g["tol"])), observables=tuple(specs), diag=diag)
+    return rs.evolve_sv(seq, reg, cfg)
+
+
+class TestEvolve:
+    @pytest.mark.parametrize("case", ["ring10", "adiabatic5", "adiabatic9", "random0", "random1", "random2",
+                                      "blockade2", "detmap12"])
+    @pytest.mark.parametrize("diag", ["fly", "vec"])
+    def test_golden_evolutions(self, rs, case, diag):
+        g = load(f"evolve_{case}.npz")
+        pairs = g["pairs"] if "pairs" in g.files else ()
+        res = run_gpu(rs, g, int(g["every"]), pairs, energy=True, diag=diag)
+        psi = res.final_state.cpu().numpy()
+        ref = g["final_state"]
+        fid = abs(np.vdot(ref, psi)) ** 2
+        assert 1.0 - fid <= 1e-10
+        assert np.linalg.norm(psi - ref) <= 1e-8
+        occ = np.array([r.values for r in res.observables if r.kind == "occupation"])
+        assert occ.shape == g["occ"].shape
+        assert np.abs(occ - g["occ"]).max() <= 1e-8
+        if len(pairs):
+            corr = [r.values for r in res.observables if r.kind == "correlation"][-1]
+            assert np.abs(np.array(corr) - g["corr"]).max() <= 1e-8
+        e = [r.values[0] for r in res.observables if r.kind == "energy"][-1]
+        assert abs(e - float(g["energy_last"])) <= 1e-8 * max(1.0, abs(float(g["energy_last"])))
+        iters = np.array([r.iterations for r in res.krylov_reports])
+        assert np.abs(iters - g["iterations"]).max() <= 1
+
+    def test_lattice20_config1(self, rs):
+        g = load("evolve_lattice20.npz")
+        res = run_gpu(rs, g, 1)
+        psi = res.final_state.cpu().numpy()
+        rng = np.random.default_rng(77)
+        probe = rng.standard_normal(2 ** 20) + 1j * rng.standard_normal(2 ** 20)
+        assert abs(np.vdot(probe, psi) - complex(g["probe_overlap"])) <= 1e-8 * abs(complex(g["probe_overlap"]))
+        assert np.abs(psi[:64] - g["amp_head"]).max() <= 1e-9
+        occ = np.array([r.values for r in res.observables])
+        assert np.abs(occ - g["occ"]).max() <= 1e-8
+
+    def test_krylov_cap_substepping_is_exact(self, rs, torch):
+        # a tiny HBM budget caps the Krylov basis; the step is split in time and must agree
+        g = load("evolve_detmap12.npz")
+        n = 12
+        reg = rs.Register(tuple(map(tuple, g["positions"])), float(g["c6"]))
+        seq = rs.DiscretizedSequence(10, g["omegas"][:5], g["deltas"][:5], 50)
+        full = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12)))
+        capped = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12), krylov_vectors_cap=6))
+        assert any(r.substeps > 1 for r in capped.krylov_reports)
+        assert rs.norm_difference(full.final_state, capped.final_state) <= 1e-9
+
+    def test_rabi_analytic(self, rs):
+        seq = rs.discretize(rs.sample_program(rs.ChannelProgram.from_channels(
+            [[rs.Constant(500, 2 * np.pi)]], [[rs.Constant(500, 0.0)]], 500)), 1)
+        reg = rs.Register(((0.0, 0.0),), 1.0)
+        res = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12),
+                                                    observables=(rs.ObservableSpec("occupation", (0,)),)))
+        t = np.array([r.t_ns for r in res.observables]) * 1e-3
+        v = np.array([r.values[0] for r in res.observables])
+        assert np.abs(v - np.sin(np.pi * t) ** 2).max() <= 1e-10
+
+    def test_errors(self, rs):
+        seq = rs.DiscretizedSequence(10, np.ones((1, 4)), np.zeros((1, 4)), 10)
+        reg = rs.Register(tuple((1e6 * i, 0.0) for i in range(4)), 1.0)
+        with pytest.raises(rs.ValidationError):
+            rs.evolve_sv(seq, reg, rs.SvRunConfig(qubit_cap=3))
+        seq2 = rs.DiscretizedSequence(100, np.full((1, 2), 300.0), np.full((1, 2), -500.0), 100)
+        reg2 = rs.Register(((0.0, 0.0), (1e6, 0.0)), 1.0)
+        with pytest.raises(rs.SolverError) as err:
+            rs.evolve_sv(seq2, reg2, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12, max_krylov_dim=2)))
+        assert err.value.step == 0
+
+
+class TestObservables:
+    def test_against_oracle(self, rs):
+        rng = np.random.default_rng(4)
+        for n in (3, 9, 15):
+            psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+            occ = rs.occupations(psi)
+            assert np.abs(occ - O.occupations(psi)).max() <= 1e-13
+            assert abs(rs.correlation(psi, 0, n - 1) - O.correlation(psi, 0, n - 1)) <= 1e-13
+            phi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+            assert abs(rs.overlap(psi, phi) - np.vdot(psi, phi)) <= 1e-10 * abs(np.vdot(psi, phi))
+            assert abs(rs.norm_difference(psi, phi) - np.linalg.norm(psi - phi)) <= 1e-12 * np.linalg.norm(psi)
