@@ -35,10 +35,21 @@ __device__ __forceinline__ uint64_t tile_index(const Shape& sh, uint64_t t, uint
   return (uint64_t)lo | (tmid << sh.a) | (h << sh.p) | (thi << (sh.p + sh.g));
 }
 
-template <int NW>
-__device__ __forceinline__ double block_sum(double v, double* red) {
+// Sum over the lanes of a (possibly partial, NT < 32) warp.
+template <int NT>
+__device__ __forceinline__ double warp_sum(double v) {
+  constexpr unsigned mask = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
+  constexpr int top = NT >= 32 ? 16 : NT / 2;
   #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = top; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+// Block-wide sum for a CTA of exactly NT threads; every thread gets the result.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  constexpr int NW = (NT + 31) / 32;
+  v = warp_sum<NT>(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
   if (l == 0) red[w] = v;
@@ -52,7 +63,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // Deterministic grid reduction: every CTA writes its row, the last CTA to
 // arrive sums the rows in index order. Returns true in the last CTA, where
 // `tot` then holds the column sums.
-template <int NCOL>
+template <int NCOL, int NT>
 __device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned* counter,
                               double (&tot)[NCOL], double* red) {
   __shared__ bool s_last;
@@ -69,8 +80,8 @@ __device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned
   #pragma unroll
   for (int c = 0; c < NCOL; ++c) {
     double v = 0.0;
-    for (unsigned r = threadIdx.x; r < gridDim.x; r += blockDim.x) v += __ldcg(part + (size_t)r * NCOL + c);
-    tot[c] = block_sum<kThreads / 32>(v, red);
+    for (unsigned r = threadIdx.x; r < gridDim.x; r += NT) v += __ldcg(part + (size_t)r * NCOL + c);
+    tot[c] = block_sum<NT>(v, red);
   }
   if (threadIdx.x == 0) *counter = 0u;
   return true;
@@ -86,9 +97,10 @@ struct DiagTile {
   double gc[kLoBits];
 };
 
+template <int NT>
 __device__ void diag_tile_setup(const DiagArgs& dg, const Shape& sh, uint64_t tile, DiagTile* dt) {
   const int n = sh.n, a = sh.a;
-  const uint64_t hb = tile;   // bits a..n-1 of the global index
+  const uint64_t hb = tile;   // bits a..n-1 of the global index (n - a <= 32 hi qubits, NT >= 32 whenever n > a)
   if (threadIdx.x < 32) {
     const int l = threadIdx.x;
     // hi part: detuning and hi-hi interactions, one hi qubit per lane (n - a <= 32)
@@ -101,8 +113,7 @@ __device__ void diag_tile_setup(const DiagArgs& dg, const Shape& sh, uint64_t ti
           if ((hb >> (i - a)) & 1ull) v += __ldg(dg.umat + (size_t)i * n + j);
       }
     }
-    #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    v = warp_sum<NT>(v);
     if (l == 0) dt->dh = v;
     if (l < kLoBits) {
       double gsum = 0.0;
@@ -114,9 +125,9 @@ __device__ void diag_tile_setup(const DiagArgs& dg, const Shape& sh, uint64_t ti
     }
   }
   __syncthreads();
-  if (threadIdx.x < 128) {
-    const int m = threadIdx.x & 63;
-    const int half = threadIdx.x >> 6;
+  for (int idx = threadIdx.x; idx < 128; idx += NT) {
+    const int m = idx & 63;
+    const int half = idx >> 6;
     double s = 0.0;
     #pragma unroll
     for (int b = 0; b < 6; ++b)
@@ -140,7 +151,6 @@ pass_kernel(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int NT = TILE < kThreads ? TILE : kThreads;
   constexpr int EPT = TILE / NT;
-  constexpr int NW = (NT + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* s = reinterpret_cast<cplx*>(smem_raw);
   __shared__ DiagTile dtile;
@@ -163,7 +173,7 @@ pass_kernel(const __grid_constant__ PassArgs A) {
       const uint32_t e = tid + i * NT;
       cp_async16(&s[e], A.x + tile_index(A.sh, t, e));
     }
-    if (has_diag) diag_tile_setup(A.dg, A.sh, t, &dtile);
+    if (has_diag) diag_tile_setup<NT>(A.dg, A.sh, t, &dtile);
     cp_async_wait_all();
     __syncthreads();
 
@@ -234,11 +244,11 @@ pass_kernel(const __grid_constant__ PassArgs A) {
 
   if (KIND == PASS_LAST_APPLY) return;
   double mine[3];
-  mine[0] = block_sum<NW>(acc_a, red);
-  mine[1] = block_sum<NW>(acc_n, red);
-  mine[2] = block_sum<NW>(acc_q, red);
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = block_sum<NT>(acc_n, red);
+  mine[2] = block_sum<NT>(acc_q, red);
   double tot[3];
-  if (!grid_finalize<3>(mine, A.part, A.counter, tot, red)) return;
+  if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
   if (threadIdx.x != 0) return;
   double* scw = A.sc;
   if (KIND == PASS_FIRST) {
@@ -263,7 +273,6 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int NT = TILE < kThreads ? TILE : kThreads;
   constexpr int EPT = TILE / NT;
-  constexpr int NW = (NT + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* s = reinterpret_cast<cplx*>(smem_raw);
   __shared__ DiagTile dtile;
@@ -275,7 +284,7 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
   double acc_n = 0.0, acc_q = 0.0;
 
   for (uint64_t t = blockIdx.x; t < A.sh.n_tiles; t += gridDim.x) {
-    if (has_diag) diag_tile_setup(A.dg, A.sh, t, &dtile);
+    if (has_diag) diag_tile_setup<NT>(A.dg, A.sh, t, &dtile);
     cplx wv[EPT];
     #pragma unroll
     for (int i = 0; i < EPT; ++i) wv[i] = make_double2(0.0, 0.0);
@@ -336,7 +345,7 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
         }
         #pragma unroll
         for (int mm = 0; mm < 8; ++mm) {
-          const double v = block_sum<NW>(acc[mm], red);
+          const double v = block_sum<NT>(acc[mm], red);
           if (tid == 0 && m0 + mm < A.nmask) s_obs[m0 + mm] += v;
         }
       }
@@ -345,8 +354,8 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
   }
 
   double mine[2];
-  mine[0] = block_sum<NW>(acc_n, red);
-  mine[1] = block_sum<NW>(acc_q, red);
+  mine[0] = block_sum<NT>(acc_n, red);
+  mine[1] = block_sum<NT>(acc_q, red);
   __syncthreads();
   // write observables as extra rows: reuse the generic finalize with a fixed column count
   __shared__ bool s_last;
@@ -369,7 +378,7 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
   for (int c = 0; c < ncol; ++c) {
     double v = 0.0;
     for (unsigned r = tid; r < gridDim.x; r += NT) v += __ldcg(A.part + (size_t)r * (2 + kMaxMasks) + c);
-    const double sum = block_sum<NW>(v, red);
+    const double sum = block_sum<NT>(v, red);
     if (c < 2) tot[c] = sum;
     else if (tid == 0) A.sc[SC_OBS + c - 2] = sum;   // raw sums; host divides by ||psi||^2
   }
@@ -426,9 +435,9 @@ __global__ void zdotc_kernel(const cplx* __restrict__ x, const cplx* __restrict_
     re = fma(a.x, b.x, fma(a.y, b.y, re));   // conj(a) * b
     im = fma(a.x, b.y, fma(-a.y, b.x, im));
   }
-  double mine[2] = {block_sum<kThreads / 32>(re, red), block_sum<kThreads / 32>(im, red)};
+  double mine[2] = {block_sum<kThreads>(re, red), block_sum<kThreads>(im, red)};
   double tot[2];
-  if (!grid_finalize<2>(mine, part, counter, tot, red)) return;
+  if (!grid_finalize<2, kThreads>(mine, part, counter, tot, red)) return;
   if (threadIdx.x == 0) { result2[0] = tot[0]; result2[1] = tot[1]; }
 }
 
@@ -442,9 +451,9 @@ __global__ void diff_norm_kernel(const cplx* __restrict__ x, const cplx* __restr
     const double dr = a.x - b.x, di = a.y - b.y;
     s = fma(dr, dr, fma(di, di, s));
   }
-  double mine[1] = {block_sum<kThreads / 32>(s, red)};
+  double mine[1] = {block_sum<kThreads>(s, red)};
   double tot[1];
-  if (!grid_finalize<1>(mine, part, counter, tot, red)) return;
+  if (!grid_finalize<1, kThreads>(mine, part, counter, tot, red)) return;
   if (threadIdx.x == 0) result[0] = tot[0];
 }
 
@@ -462,9 +471,9 @@ __global__ void lanczos_update_kernel(cplx* __restrict__ w, const cplx* __restri
     w[i] = a;
     nn = fma(a.x, a.x, fma(a.y, a.y, nn));
   }
-  double mine[1] = {block_sum<kThreads / 32>(nn, red)};
+  double mine[1] = {block_sum<kThreads>(nn, red)};
   double tot[1];
-  if (!grid_finalize<1>(mine, part, counter, tot, red)) return;
+  if (!grid_finalize<1, kThreads>(mine, part, counter, tot, red)) return;
   if (threadIdx.x == 0) result[0] = tot[0];
 }
 
