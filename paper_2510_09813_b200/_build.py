@@ -31,18 +31,18 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, target: str = TARGET, defines=()) -> str:
+    if not force and target == TARGET and not needs_build():
         return TARGET
     cmd = [nvcc_path(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3",
            "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"),
-           "-o", TARGET + ".tmp", *SOURCES]
+           *[f"-D{d}" for d in defines], "-o", target + ".tmp", *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(TARGET + ".tmp", TARGET)
-    return TARGET
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

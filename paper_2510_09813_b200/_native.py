@@ -14,7 +14,8 @@ import threading
 from .errors import RydsimError, SolverError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_rsv.so")
+# RSV_LIB overrides the library path (used to A/B compile-time kernel variants in tools/)
+LIB_PATH = os.environ.get("RSV_LIB") or os.path.join(_HERE, "_rsv.so")
 
 RSV_OK = 0
 RSV_ERR_ARG = -1

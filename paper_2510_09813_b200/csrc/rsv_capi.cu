@@ -157,6 +157,7 @@ struct rsv_context {
   double* d_part = nullptr;
   unsigned* d_counter = nullptr;
   double* d_dl = nullptr;
+  double* d_gc = nullptr;         // lo-pass tile table (per run)
   double* d_dvec = nullptr;
   double* h_pin = nullptr;
   std::vector<void*> phys;        // bound slots
@@ -201,7 +202,7 @@ void build_plan(rsv_context* c) {
   c->plan.push_back(lo);
   const int rem = n - alo;
   if (rem <= 0) return;
-  const int gmax = 10;   // hi tile = 2^(12-g) contiguous x 2^g strided, runs >= 64 B
+  const int gmax = rsv::kLoBits - 2;   // hi tile = 2^(TB-g) contiguous x 2^g strided, runs >= 64 B
   const int ng = (rem + gmax - 1) / gmax;
   std::vector<int> sizes;
   for (int i = 0; i < ng; ++i) sizes.push_back(rem / ng + (i < rem % ng ? 1 : 0));   // descending
@@ -218,16 +219,24 @@ void build_plan(rsv_context* c) {
   }
 }
 
-rsv::FlipSet flips_for(const PassPlan& p, const double* omegas) {
+rsv::FlipSet flips_for(const PassPlan& p, const double* omegas, int kind) {
+  // Tile bits below log2(threads per CTA) are flipped through shared memory, the
+  // ones above are register permutations inside a thread (pass_kernel, RegBits).
   rsv::FlipSet f{};
   f.count = 0;
+  const int tb = p.sh.a + p.sh.g;
+  const int lt = rsv::ilog2(rsv::pass_threads(tb, kind));
   for (int q = p.q0; q < p.q0 + p.nq; ++q) {
     const double cq = 0.5 * omegas[q];
     if (cq == 0.0) continue;   // zero drives are skipped, as in _kernels.py:19
     const int local = p.lo ? q : p.sh.a + (q - p.sh.p);
-    f.mask[f.count] = 1 << local;
-    f.coef[f.count] = cq;
-    ++f.count;
+    if (local >= lt) {
+      f.rcoef[local - lt] = cq;
+    } else {
+      f.mask[f.count] = 1 << local;
+      f.coef[f.count] = cq;
+      ++f.count;
+    }
   }
   return f;
 }
@@ -238,6 +247,7 @@ rsv::DiagArgs diag_for(const rsv_context* c, const PassPlan& p, const double* de
   if (!p.lo) return d;
   d.mode = c->diag_mode == RSV_DIAG_VEC ? rsv::DIAG_VEC : rsv::DIAG_FLY;
   d.dl = c->d_dl;
+  d.gc = c->d_gc;
   d.umat = c->d_u;
   d.dvec = c->d_dvec;
   for (int i = 0; i < c->n; ++i) d.delta[i] = deltas[i];
@@ -248,8 +258,8 @@ int ensure_dl(rsv_context* c, const double* deltas) {
   const int alo = c->plan[0].sh.a;
   std::vector<double> key(deltas, deltas + alo);
   if (c->dl_valid && key == c->dl_key) return RSV_OK;
-  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, nullptr, deltas, c->diag_mode == RSV_DIAG_FLY ? 1 : 0,
-                                c->d_dl, c->st));
+  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, deltas, c->diag_mode == RSV_DIAG_FLY ? 1 : 0, c->d_dl,
+                                c->st));
   c->dl_key = key;
   c->dl_valid = true;
   return RSV_OK;
@@ -305,7 +315,7 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
   A.sh = last.sh;
   A.qsweep = q_omegas != nullptr ? 1 : 0;
   if (A.qsweep) {
-    A.fl = flips_for(last, q_omegas);
+    A.fl = flips_for(last, q_omegas, rsv::PASS_FIRST);   // combine CTAs use the FIRST-pass thread count
     A.dg = diag_for(c, last, q_deltas);
     if (last.lo) {
       int rc = ensure_dl(c, q_deltas);
@@ -328,7 +338,7 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
   A.part = c->d_part;
   A.counter = c->d_counter;
   prof_begin(c, 3);
-  CUDA_TRY(rsv::launch_combine(A, rsv::pass_grid(A.sh), c->st));
+  CUDA_TRY(rsv::launch_combine(A, c->st));
   prof_end(c);
   if (A.nmask > 0) {
     CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_OBS, c->d_sc + rsv::SC_OBS, sizeof(double) * A.nmask,
@@ -356,8 +366,10 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
   for (size_t pi = 0; pi < np; ++pi) {
     const PassPlan& p = c->plan[pi];
     rsv::PassArgs A{};
+    const bool last = pi + 1 == np;
+    A.kind = last ? rsv::PASS_LAST_LANCZOS : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
-    A.fl = flips_for(p, omegas);
+    A.fl = flips_for(p, omegas, A.kind);
     A.dg = diag_for(c, p, deltas);
     A.x = slot(c, j);
     A.x_scale_slot = rsv::SC_SG + j;
@@ -365,20 +377,17 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     A.sc = c->d_sc;
     A.part = c->d_part;
     A.counter = c->d_counter;
-    const bool last = pi + 1 == np;
     if (!last) {
-      A.kind = pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID;
       A.uin = pi == 0 ? nullptr : work(c);
       A.out = work(c);
     } else {
-      A.kind = rsv::PASS_LAST_LANCZOS;
       A.uin = np > 1 ? work(c) : nullptr;
       A.out = slot(c, j + 1);
       A.prev = j > 0 ? slot(c, j - 1) : nullptr;
       A.qsweep = 1;
     }
     prof_begin(c, family_of(pi, np));
-    CUDA_TRY(rsv::launch_pass(A, rsv::pass_grid(A.sh), c->st));
+    CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
   }
   return RSV_OK;
@@ -534,13 +543,16 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
   cudaGetDevice(&c->device);
   c->h_u.assign(interaction_u, interaction_u + (size_t)n_qubits * n_qubits);
   build_plan(c);
-  int maxgrid = rsv::max_pass_grid(rsv::kLoBits) * 2;
+  const int maxgrid = rsv::max_grid_rows();
+  const int alo = std::min(n_qubits, rsv::kLoBits);
+  const size_t gc_rows = size_t(1) << (n_qubits - alo);
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = cudaMalloc(&c->d_u, sizeof(double) * n_qubits * n_qubits);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_sc, sizeof(double) * rsv::SC_SIZE);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_part, sizeof(double) * (size_t)maxgrid * kPartStride);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_dl, sizeof(double) << rsv::kLoBits);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_gc, sizeof(double) * rsv::kGcStride * gc_rows);
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_pin, sizeof(double) * rsv::SC_SIZE);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->obs_event, cudaEventDisableTiming);
   if (e == cudaSuccess)
@@ -549,6 +561,8 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
   if (e == cudaSuccess) e = cudaMemset(c->d_sc, 0, sizeof(double) * rsv::SC_SIZE);
   double one = 1.0;
   if (e == cudaSuccess) e = cudaMemcpy(c->d_sc + rsv::SC_ONE, &one, sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = rsv::launch_tile_table(alo, n_qubits, c->d_u, c->d_gc, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     rsv_destroy(c);
     return fail(RSV_ERR_CUDA, "rsv_create: %s", cudaGetErrorString(e));
@@ -564,6 +578,7 @@ void rsv_destroy(rsv_context* c) {
   cudaFree(c->d_part);
   cudaFree(c->d_counter);
   cudaFree(c->d_dl);
+  cudaFree(c->d_gc);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->obs_event) cudaEventDestroy(c->obs_event);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -632,8 +647,9 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
   for (size_t pi = 0; pi < np; ++pi) {
     const PassPlan& p = c->plan[pi];
     rsv::PassArgs A{};
+    A.kind = pi + 1 == np ? rsv::PASS_LAST_APPLY : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
-    A.fl = flips_for(p, omegas);
+    A.fl = flips_for(p, omegas, A.kind);
     A.dg = diag_for(c, p, deltas);
     A.x = reinterpret_cast<const cplx*>(psi);
     A.x_scale_slot = rsv::SC_ONE;
@@ -643,14 +659,12 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     A.counter = c->d_counter;
     A.out = reinterpret_cast<cplx*>(out);
     if (pi + 1 == np) {
-      A.kind = rsv::PASS_LAST_APPLY;
       A.uin = np > 1 ? reinterpret_cast<const cplx*>(out) : nullptr;
     } else {
-      A.kind = pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID;
       A.uin = pi == 0 ? nullptr : reinterpret_cast<const cplx*>(out);
     }
     prof_begin(c, family_of(pi, np));
-    CUDA_TRY(rsv::launch_pass(A, rsv::pass_grid(A.sh), c->st));
+    CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
   }
   return RSV_OK;
@@ -737,7 +751,7 @@ int rsv_observe(rsv_context* c, const void* psi, const uint64_t* masks, int nmas
   A.part = c->d_part;
   A.counter = c->d_counter;
   // the combine overwrites SC_N0SQ / SC_SG / SC_Q: the resident state is re-prepared on its next step
-  CUDA_TRY(rsv::launch_combine(A, rsv::pass_grid(A.sh), c->st));
+  CUDA_TRY(rsv::launch_combine(A, c->st));
   CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_OBS, c->d_sc + rsv::SC_OBS, sizeof(double) * (nmask > 0 ? nmask : 1),
                            cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_SIZE - 3, c->d_sc + rsv::SC_N0SQ, sizeof(double), cudaMemcpyDeviceToHost, c->st));

@@ -1,19 +1,23 @@
-// rsv_kernels.cu -- see rsv_kernels.cuh for the design notes.
+// rsv_kernels.cu -- sm_100a kernels; see rsv_kernels.cuh for the design notes.
 #include "rsv_kernels.cuh"
+
+#ifndef RSV_STAGES
+#define RSV_STAGES 2
+#endif
 
 namespace rsv {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;     // generic / combine kernels
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ cplx ld_stream(const cplx* p) {
   // streaming 128-bit load (evict-first). Coherent path on purpose: the
@@ -21,8 +25,7 @@ __device__ __forceinline__ cplx ld_stream(const cplx* p) {
   return __ldcs(p);
 }
 __device__ __forceinline__ void st_stream(cplx* p, cplx v) {
-  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y)
-               : "memory");
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
 // Global index of tile-local element e in tile t.
@@ -34,8 +37,14 @@ __device__ __forceinline__ uint64_t tile_index(const Shape& sh, uint64_t t, uint
   const uint64_t thi = t >> m;
   return (uint64_t)lo | (tmid << sh.a) | (h << sh.p) | (thi << (sh.p + sh.g));
 }
+// Offset of tile element e relative to element 0 of the same tile (the fields are disjoint,
+// so index(t, tid + i*NT) = index(t, tid) + offset(i*NT)).
+__device__ __forceinline__ uint64_t elem_offset(const Shape& sh, uint32_t e) {
+  const uint32_t lo = e & ((1u << sh.a) - 1u);
+  const uint64_t h = e >> sh.a;
+  return (uint64_t)lo | (h << sh.p);
+}
 
-// Sum over the lanes of a (possibly partial, NT < 32) warp.
 template <int NT>
 __device__ __forceinline__ double warp_sum(double v) {
   constexpr unsigned mask = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
@@ -60,12 +69,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// Deterministic grid reduction: every CTA writes its row, the last CTA to
-// arrive sums the rows in index order. Returns true in the last CTA, where
-// `tot` then holds the column sums.
+// Deterministic grid reduction: every CTA writes its row, the last CTA to arrive sums the
+// rows in index order. Returns true in the last CTA, where `tot` holds the column sums.
 template <int NCOL, int NT>
-__device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned* counter,
-                              double (&tot)[NCOL], double* red) {
+__device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned* counter, double (&tot)[NCOL],
+                              double* red) {
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
     #pragma unroll
@@ -87,73 +95,73 @@ __device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned
   return true;
 }
 
-// Per-tile diagonal helpers for the lo tile (bits [0, a) contiguous, g == 0).
-// d[b] = dl[lo] + dh(tile) + sum_{i<a} bit_i(lo) * gcross_i(tile)
-// gcross_i = sum_{j>=a} U_ij bit_j ; t1/t2 tabulate the cross sum on 6-bit halves.
-struct DiagTile {
-  double dh;
-  double t1[64];
-  double t2[64];
-  double gc[kLoBits];
+template <int EPT>
+struct RegBits {
+  static constexpr int value = EPT >= 16 ? 4 : (EPT >= 8 ? 3 : (EPT >= 4 ? 2 : (EPT >= 2 ? 1 : 0)));
+};
+template <int N>
+struct Log2 {
+  static constexpr int value = N <= 1 ? 0 : 1 + Log2<N / 2>::value;
 };
 
-template <int NT>
-__device__ void diag_tile_setup(const DiagArgs& dg, const Shape& sh, uint64_t tile, DiagTile* dt) {
-  const int n = sh.n, a = sh.a;
-  const uint64_t hb = tile;   // bits a..n-1 of the global index (n - a <= 32 hi qubits, NT >= 32 whenever n > a)
-  if (threadIdx.x < 32) {
-    const int l = threadIdx.x;
-    // hi part: detuning and hi-hi interactions, one hi qubit per lane (n - a <= 32)
-    double v = 0.0;
-    const int j = a + l;
-    if (j < n && ((hb >> l) & 1ull)) {
-      v = -dg.delta[j];
-      if (dg.mode == DIAG_FLY) {
-        for (int i = a; i < j; ++i)
-          if ((hb >> (i - a)) & 1ull) v += __ldg(dg.umat + (size_t)i * n + j);
-      }
+// ---------------------------------------------------------------- on-the-fly diagonal
+// For the lo tile (bits [0, a) contiguous, tile t = bits a..n-1):
+//   d(b) = dl[e] + hh[t] - sum_{j>=a} delta_j bit_j(t) + sum_{i<a} bit_i(e) gc[t][i]
+// dl (2^a, per step): lo detuning (+ lo-lo interactions for DIAG_FLY);
+// hh, gc (per run, DIAG_FLY): hi-hi interactions and the lo-hi couplings of tile t.
+// Thread tid owns e_i = tid + i*NT, so the cross term splits into a per-thread part
+// (bits of tid) and a per-element part (bits of i): no shared tables, no barriers.
+template <int NT, int EPT>
+struct DiagRow {
+  double d[EPT];
+
+  __device__ __forceinline__ void setup(const DiagArgs& dg, const Shape& sh, uint64_t t, int tid) {
+    constexpr int LT = Log2<NT>::value;
+    constexpr int RB = RegBits<EPT>::value;
+    const int a = sh.a, n = sh.n;
+    double base = 0.0;
+    for (int j = a; j < n; ++j)
+      if ((t >> (j - a)) & 1ull) base -= dg.delta[j];
+    double cross_t = 0.0;
+    double gy[RB > 0 ? RB : 1];
+    if (dg.mode == DIAG_FLY) {
+      const double* g = dg.gc + t * kGcStride;
+      base += __ldg(g + kGcStride - 1);   // hh[t] stored in the last column
+      #pragma unroll
+      for (int b = 0; b < LT; ++b)
+        if (b < a && ((tid >> b) & 1)) cross_t += __ldg(g + b);
+      #pragma unroll
+      for (int b = 0; b < RB; ++b) gy[b] = (LT + b < a) ? __ldg(g + LT + b) : 0.0;
+    } else {
+      #pragma unroll
+      for (int b = 0; b < RB; ++b) gy[b] = 0.0;
     }
-    v = warp_sum<NT>(v);
-    if (l == 0) dt->dh = v;
-    if (l < kLoBits) {
-      double gsum = 0.0;
-      if (dg.mode == DIAG_FLY && l < a) {
-        for (int jj = a; jj < n; ++jj)
-          if ((hb >> (jj - a)) & 1ull) gsum += __ldg(dg.umat + (size_t)l * n + jj);
-      }
-      dt->gc[l] = gsum;
-    }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < 128; idx += NT) {
-    const int m = idx & 63;
-    const int half = idx >> 6;
-    double s = 0.0;
     #pragma unroll
-    for (int b = 0; b < 6; ++b)
-      if ((m >> b) & 1) s += dt->gc[half * 6 + b];
-    if (half == 0) dt->t1[m] = s; else dt->t2[m] = s;
+    for (int i = 0; i < EPT; ++i) {
+      double v = base + cross_t + __ldg(dg.dl + tid + i * NT);
+      #pragma unroll
+      for (int b = 0; b < RB; ++b)
+        if ((i >> b) & 1) v += gy[b];
+      d[i] = v;
+    }
   }
-  // caller syncs
-}
+};
 
-__device__ __forceinline__ double diag_value(const DiagArgs& dg, const DiagTile* dt, uint32_t e,
-                                             uint64_t gi) {
-  double d = __ldg(dg.dl + e) + dt->dh;
-  if (dg.mode == DIAG_FLY) d += dt->t1[e & 63] + dt->t2[(e >> 6) & 63];
-  else d += __ldg(dg.dvec + gi);
-  return d;
-}
-
-template <int TB, int KIND>
-__global__ void __launch_bounds__((1 << TB) < kThreads ? (1 << TB) : kThreads, 2)
-pass_kernel(const __grid_constant__ PassArgs A) {
+// ---------------------------------------------------------------- bit-group pass
+// Persistent CTAs walk tiles t = blockIdx.x + k*gridDim.x. The x tile goes through a ring
+// of STAGES shared-memory buffers filled by cp.async one ring ahead; the elementwise
+// operands (uin, prev) are prefetched into registers at the top of each iteration. Thread
+// tid owns tile elements e_i = tid + i*NT: flips on tile bits >= log2(NT) are register
+// permutations, the others one conflict-free 16-byte shared load per element.
+template <int TB, int KIND, int NT>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
-  constexpr int NT = TILE < kThreads ? TILE : kThreads;
   constexpr int EPT = TILE / NT;
+  constexpr int RB = RegBits<EPT>::value;
+  constexpr int STAGES = TB >= 8 ? RSV_STAGES : 2;
+  constexpr bool LANCZOS = KIND == PASS_LAST_LANCZOS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* s = reinterpret_cast<cplx*>(smem_raw);
-  __shared__ DiagTile dtile;
+  cplx* sbuf = reinterpret_cast<cplx*>(smem_raw);   // STAGES x TILE
   __shared__ double red[32];
 
   const int tid = threadIdx.x;
@@ -161,86 +169,148 @@ pass_kernel(const __grid_constant__ PassArgs A) {
   const double xs = sc[A.x_scale_slot];
   const bool has_diag = A.dg.mode != DIAG_NONE;
   double alpha = 0.0, bprev = 0.0;
-  if (KIND == PASS_LAST_LANCZOS) {
+  if (LANCZOS) {
     alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
     if (A.prev != nullptr && A.j > 0) bprev = sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1];
   }
+  double rc[RB > 0 ? RB : 1];
+  #pragma unroll
+  for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b];
+  const bool has_u = KIND != PASS_FIRST && A.uin != nullptr;
+  const bool has_prev = LANCZOS && bprev != 0.0;
   double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
+  uint64_t off[EPT];
+  #pragma unroll
+  for (int i = 0; i < EPT; ++i) off[i] = elem_offset(A.sh, i * NT);
 
-  for (uint64_t t = blockIdx.x; t < A.sh.n_tiles; t += gridDim.x) {
-    #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const uint32_t e = tid + i * NT;
-      cp_async16(&s[e], A.x + tile_index(A.sh, t, e));
+  const uint64_t ntiles = A.sh.n_tiles;
+  const uint64_t G = gridDim.x;
+  #pragma unroll
+  for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+    const uint64_t tp = blockIdx.x + (uint64_t)s0 * G;
+    if (tp < ntiles) {
+      const cplx* src = A.x + tile_index(A.sh, tp, tid);
+      cplx* dst = sbuf + s0 * TILE + tid;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) cp_async16(dst + i * NT, src + off[i]);
     }
-    if (has_diag) diag_tile_setup<NT>(A.dg, A.sh, t, &dtile);
-    cp_async_wait_all();
+    cp_async_commit();
+  }
+  int stage = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += G, stage = (stage + 1 == STAGES ? 0 : stage + 1)) {
+    const uint64_t g0 = tile_index(A.sh, t, tid);
+    const uint64_t tn = t + (uint64_t)(STAGES - 1) * G;
+    if (tn < ntiles) {
+      const cplx* src = A.x + tile_index(A.sh, tn, tid);
+      cplx* dst = sbuf + (stage == 0 ? STAGES - 1 : stage - 1) * TILE + tid;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) cp_async16(dst + i * NT, src + off[i]);
+    }
+    cp_async_commit();
+    cplx uv[EPT], pv[EPT];
+    if (has_u) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) uv[i] = ld_stream(A.uin + g0 + off[i]);
+    }
+    if (has_prev) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) pv[i] = ld_stream(A.prev + g0 + off[i]);
+    }
+    DiagRow<NT, EPT> dr;
+    if (has_diag) dr.setup(A.dg, A.sh, t, tid);
+    cp_async_wait<STAGES - 1>();
     __syncthreads();
+    cplx* s = sbuf + stage * TILE;
 
-    cplx wv[EPT];
+    cplx xv[EPT], ac[EPT];
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-      const uint32_t e = tid + i * NT;
-      const uint64_t gi = tile_index(A.sh, t, e);
-      const cplx xv = s[e];
-      double cr = 0.0, ci = 0.0;
-      for (int f = 0; f < A.fl.count; ++f) {
-        const cplx pv = s[e ^ A.fl.mask[f]];
-        cr = fma(A.fl.coef[f], pv.x, cr);
-        ci = fma(A.fl.coef[f], pv.y, ci);
+      xv[i] = s[tid + i * NT];
+      ac[i] = make_double2(0.0, 0.0);
+    }
+    #pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        ac[i].x = fma(rc[b], xv[i ^ (1 << b)].x, ac[i].x);
+        ac[i].y = fma(rc[b], xv[i ^ (1 << b)].y, ac[i].y);
       }
-      if (has_diag) {
-        const double d = diag_value(A.dg, &dtile, e, gi);
-        cr = fma(d, xv.x, cr);
-        ci = fma(d, xv.y, ci);
+    }
+    for (int f = 0; f < A.fl.count; ++f) {
+      const int m = A.fl.mask[f];
+      const double c = A.fl.coef[f];
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const cplx p = s[(tid + i * NT) ^ m];
+        ac[i].x = fma(c, p.x, ac[i].x);
+        ac[i].y = fma(c, p.y, ac[i].y);
       }
-      cr *= xs; ci *= xs;   // contribution of this pass's operator applied to v = xs * x
-      // <v | contribution>, real part
-      acc_a = fma(xs * xv.x, cr, fma(xs * xv.y, ci, acc_a));
-      double orr = cr, oi = ci;
-      if (A.uin != nullptr) {
-        const cplx u = ld_stream(A.uin + gi);
-        orr += u.x; oi += u.y;
+    }
+    if (has_diag) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        double d = dr.d[i];
+        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + off[i]);
+        ac[i].x = fma(d, xv[i].x, ac[i].x);
+        ac[i].y = fma(d, xv[i].y, ac[i].y);
       }
-      if (KIND == PASS_LAST_LANCZOS) {
-        orr = fma(-alpha * xs, xv.x, orr);
-        oi = fma(-alpha * xs, xv.y, oi);
-        if (bprev != 0.0) {
-          const cplx pv = ld_stream(A.prev + gi);
-          orr = fma(-bprev, pv.x, orr);
-          oi = fma(-bprev, pv.y, oi);
+    }
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      double cr = ac[i].x * xs, ci = ac[i].y * xs;   // this pass's operator applied to v = xs * x
+      acc_a = fma(xs * xv[i].x, cr, fma(xs * xv[i].y, ci, acc_a));
+      if (has_u) {
+        cr += uv[i].x;
+        ci += uv[i].y;
+      }
+      if (LANCZOS) {
+        cr = fma(-alpha * xs, xv[i].x, cr);
+        ci = fma(-alpha * xs, xv[i].y, ci);
+        if (has_prev) {
+          cr = fma(-bprev, pv[i].x, cr);
+          ci = fma(-bprev, pv[i].y, ci);
         }
-        acc_n = fma(orr, orr, fma(oi, oi, acc_n));
+        acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
-      if (KIND == PASS_LAST_LANCZOS) wv[i] = make_double2(orr, oi);
-      st_stream(A.out + gi, make_double2(orr, oi));
+      ac[i] = make_double2(cr, ci);
+      st_stream(A.out + g0 + off[i], ac[i]);
     }
 
-    if (KIND == PASS_LAST_LANCZOS && A.qsweep) {
-      // q-sweep: <w | A_this w> with w still on chip (this pass's share of alpha_{j+1})
+    if (LANCZOS && A.qsweep) {
+      // q-sweep: <w | A_this w> while w is on chip (this pass's share of alpha_{j+1})
       __syncthreads();
       #pragma unroll
-      for (int i = 0; i < EPT; ++i) s[tid + i * NT] = wv[i];
+      for (int i = 0; i < EPT; ++i) s[tid + i * NT] = ac[i];
       __syncthreads();
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        const uint32_t e = tid + i * NT;
-        double cr = 0.0, ci = 0.0;
-        for (int f = 0; f < A.fl.count; ++f) {
-          const cplx pv = s[e ^ A.fl.mask[f]];
-          cr = fma(A.fl.coef[f], pv.x, cr);
-          ci = fma(A.fl.coef[f], pv.y, ci);
+        double hr = 0.0, hi = 0.0;
+        #pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          hr = fma(rc[b], ac[i ^ (1 << b)].x, hr);
+          hi = fma(rc[b], ac[i ^ (1 << b)].y, hi);
         }
         if (has_diag) {
-          const double d = diag_value(A.dg, &dtile, e, tile_index(A.sh, t, e));
-          cr = fma(d, wv[i].x, cr);
-          ci = fma(d, wv[i].y, ci);
+          double d = dr.d[i];
+          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + off[i]);
+          hr = fma(d, ac[i].x, hr);
+          hi = fma(d, ac[i].y, hi);
         }
-        acc_q = fma(wv[i].x, cr, fma(wv[i].y, ci, acc_q));
+        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
+      }
+      for (int f = 0; f < A.fl.count; ++f) {
+        const int m = A.fl.mask[f];
+        const double c = A.fl.coef[f];
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const cplx p = s[(tid + i * NT) ^ m];
+          acc_q = fma(c, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
+        }
       }
     }
     __syncthreads();
   }
+  cp_async_wait<0>();
 
   if (KIND == PASS_LAST_APPLY) return;
   double mine[3];
@@ -265,106 +335,111 @@ pass_kernel(const __grid_constant__ PassArgs A) {
   }
 }
 
-// Krylov combination psi_new = sum_i coef_i v_i, fused with the next step's
-// ||psi||^2, q_0 and the observable masks.
-template <int TB>
-__global__ void __launch_bounds__((1 << TB) < kThreads ? (1 << TB) : kThreads, 2)
-combine_kernel(const __grid_constant__ CombineArgs A) {
+// ---------------------------------------------------------------- Krylov combination
+// psi_new = sum_i coef_i v_i streamed tile by tile, fused with the next step's ||psi||^2,
+// q_0 (q-sweep with the next step's coefficients) and the observable masks. Observables
+// are reduced per warp into shared rows (no block barriers inside the tile loop).
+template <int TB, int NT>
+__global__ void __launch_bounds__(NT, 2) combine_kernel(const __grid_constant__ CombineArgs A) {
   constexpr int TILE = 1 << TB;
-  constexpr int NT = TILE < kThreads ? TILE : kThreads;
   constexpr int EPT = TILE / NT;
+  constexpr int RB = RegBits<EPT>::value;
+  constexpr int NW = (NT + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* s = reinterpret_cast<cplx*>(smem_raw);
-  __shared__ DiagTile dtile;
   __shared__ double red[32];
-  __shared__ double s_obs[kMaxMasks];
-  const int tid = threadIdx.x;
+  __shared__ double s_obs[NW][kMaxMasks];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool has_diag = A.qsweep && A.dg.mode != DIAG_NONE;
-  for (int m = tid; m < A.nmask; m += NT) s_obs[m] = 0.0;
+  for (int m = lane; m < A.nmask; m += 32) s_obs[warp][m] = 0.0;
   double acc_n = 0.0, acc_q = 0.0;
+  uint64_t off[EPT];
+  #pragma unroll
+  for (int i = 0; i < EPT; ++i) off[i] = elem_offset(A.sh, i * NT);
 
   for (uint64_t t = blockIdx.x; t < A.sh.n_tiles; t += gridDim.x) {
-    if (has_diag) diag_tile_setup<NT>(A.dg, A.sh, t, &dtile);
+    const uint64_t g0 = tile_index(A.sh, t, tid);
     cplx wv[EPT];
     #pragma unroll
     for (int i = 0; i < EPT; ++i) wv[i] = make_double2(0.0, 0.0);
     for (int k = 0; k < A.k; ++k) {
-      const cplx* vk = A.v[k];
+      const cplx* vk = A.v[k] + g0;
       const double2 c = A.coef[k];
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        const cplx x = ld_stream(vk + tile_index(A.sh, t, tid + i * NT));
+        const cplx x = ld_stream(vk + off[i]);
         wv[i].x = fma(c.x, x.x, fma(-c.y, x.y, wv[i].x));
         wv[i].y = fma(c.x, x.y, fma(c.y, x.x, wv[i].y));
       }
     }
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-      const uint64_t gi = tile_index(A.sh, t, tid + i * NT);
-      if (A.out != nullptr) st_stream(A.out + gi, wv[i]);
+      if (A.out != nullptr) st_stream(A.out + g0 + off[i], wv[i]);
       acc_n = fma(wv[i].x, wv[i].x, fma(wv[i].y, wv[i].y, acc_n));
     }
     if (A.qsweep) {
+      DiagRow<NT, EPT> dr;
+      if (has_diag) dr.setup(A.dg, A.sh, t, tid);
       #pragma unroll
       for (int i = 0; i < EPT; ++i) s[tid + i * NT] = wv[i];
       __syncthreads();
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        const uint32_t e = tid + i * NT;
-        double cr = 0.0, ci = 0.0;
-        for (int f = 0; f < A.fl.count; ++f) {
-          const cplx pv = s[e ^ A.fl.mask[f]];
-          cr = fma(A.fl.coef[f], pv.x, cr);
-          ci = fma(A.fl.coef[f], pv.y, ci);
+        double hr = 0.0, hi = 0.0;
+        #pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          hr = fma(A.fl.rcoef[b], wv[i ^ (1 << b)].x, hr);
+          hi = fma(A.fl.rcoef[b], wv[i ^ (1 << b)].y, hi);
         }
         if (has_diag) {
-          const double d = diag_value(A.dg, &dtile, e, tile_index(A.sh, t, e));
-          cr = fma(d, wv[i].x, cr);
-          ci = fma(d, wv[i].y, ci);
+          double d = dr.d[i];
+          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + off[i]);
+          hr = fma(d, wv[i].x, hr);
+          hi = fma(d, wv[i].y, hi);
         }
-        acc_q = fma(wv[i].x, cr, fma(wv[i].y, ci, acc_q));
+        acc_q = fma(wv[i].x, hr, fma(wv[i].y, hi, acc_q));
       }
+      for (int f = 0; f < A.fl.count; ++f) {
+        const int m = A.fl.mask[f];
+        const double c = A.fl.coef[f];
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const cplx p = s[(tid + i * NT) ^ m];
+          acc_q = fma(c, fma(wv[i].x, p.x, wv[i].y * p.y), acc_q);
+        }
+      }
+      __syncthreads();
     }
     if (A.nmask > 0) {
       double p[EPT];
       #pragma unroll
       for (int i = 0; i < EPT; ++i) p[i] = wv[i].x * wv[i].x + wv[i].y * wv[i].y;
-      for (int m0 = 0; m0 < A.nmask; m0 += 8) {
-        double acc[8];
+      for (int m = 0; m < A.nmask; ++m) {
+        const uint64_t M = A.mask[m];
+        double v = 0.0;
         #pragma unroll
-        for (int mm = 0; mm < 8; ++mm) acc[mm] = 0.0;
-        #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-          const uint64_t gi = tile_index(A.sh, t, tid + i * NT);
-          #pragma unroll
-          for (int mm = 0; mm < 8; ++mm) {
-            const int m = m0 + mm;
-            const uint64_t M = m < A.nmask ? A.mask[m] : ~0ull;
-            acc[mm] += ((gi & M) == M) ? p[i] : 0.0;
-          }
-        }
-        #pragma unroll
-        for (int mm = 0; mm < 8; ++mm) {
-          const double v = block_sum<NT>(acc[mm], red);
-          if (tid == 0 && m0 + mm < A.nmask) s_obs[m0 + mm] += v;
-        }
+        for (int i = 0; i < EPT; ++i) v += (((g0 + off[i]) & M) == M) ? p[i] : 0.0;
+        v = warp_sum<NT>(v);
+        if (lane == 0) s_obs[warp][m] += v;
       }
     }
-    __syncthreads();
   }
 
   double mine[2];
   mine[0] = block_sum<NT>(acc_n, red);
   mine[1] = block_sum<NT>(acc_q, red);
-  __syncthreads();
-  // write observables as extra rows: reuse the generic finalize with a fixed column count
-  __shared__ bool s_last;
-  const int ncol = 2 + A.nmask;
+  constexpr int stride = 2 + kMaxMasks;
   if (tid == 0) {
-    A.part[(size_t)blockIdx.x * (2 + kMaxMasks) + 0] = mine[0];
-    A.part[(size_t)blockIdx.x * (2 + kMaxMasks) + 1] = mine[1];
+    A.part[(size_t)blockIdx.x * stride + 0] = mine[0];
+    A.part[(size_t)blockIdx.x * stride + 1] = mine[1];
   }
-  for (int m = tid; m < A.nmask; m += NT) A.part[(size_t)blockIdx.x * (2 + kMaxMasks) + 2 + m] = s_obs[m];
+  for (int m = tid; m < A.nmask; m += NT) {
+    double v = 0.0;
+    #pragma unroll
+    for (int w = 0; w < NW; ++w) v += s_obs[w][m];
+    A.part[(size_t)blockIdx.x * stride + 2 + m] = v;
+  }
+  __shared__ bool s_last;
   __threadfence();
   __syncthreads();
   if (tid == 0) {
@@ -374,13 +449,14 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  double tot[2];
+  const int ncol = 2 + A.nmask;
+  double tot[2] = {0.0, 0.0};
   for (int c = 0; c < ncol; ++c) {
     double v = 0.0;
-    for (unsigned r = tid; r < gridDim.x; r += NT) v += __ldcg(A.part + (size_t)r * (2 + kMaxMasks) + c);
+    for (unsigned r = tid; r < gridDim.x; r += NT) v += __ldcg(A.part + (size_t)r * stride + c);
     const double sum = block_sum<NT>(v, red);
     if (c < 2) tot[c] = sum;
-    else if (tid == 0) A.sc[SC_OBS + c - 2] = sum;   // raw sums; host divides by ||psi||^2
+    else if (tid == 0) A.sc[SC_OBS + c - 2] = sum;   // raw sums; the host divides by ||psi||^2
   }
   if (tid == 0) {
     *A.counter = 0u;
@@ -390,19 +466,44 @@ combine_kernel(const __grid_constant__ CombineArgs A) {
   }
 }
 
-__global__ void build_dl_kernel(int a, int n, const double* __restrict__ umat, const double* __restrict__ delta_dev,
-                                DiagArgs dg, int with_interaction, double* __restrict__ dl) {
+// ---------------------------------------------------------------- tables and helpers
+__global__ void build_dl_kernel(int a, int n, const double* __restrict__ umat, DiagArgs dg, int with_interaction,
+                                double* __restrict__ dl) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (1 << a)) return;
   double v = 0.0;
   for (int i = 0; i < a; ++i) {
     if (!((e >> i) & 1)) continue;
-    v -= delta_dev ? delta_dev[i] : dg.delta[i];
+    v -= dg.delta[i];
     if (with_interaction)
       for (int j = i + 1; j < a; ++j)
         if ((e >> j) & 1) v += umat[(size_t)i * n + j];
   }
   dl[e] = v;
+}
+
+// Per-run tile table of the lo pass: gc[t][i] = sum_{j>=a} U_ij bit_j(t) (i < a) and, in the
+// last column, hh[t] = sum_{a<=i<j} U_ij bit_i(t) bit_j(t).
+__global__ void build_tile_table_kernel(int a, int n, const double* __restrict__ umat, uint64_t ntiles,
+                                        double* __restrict__ gc) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    double* row = gc + t * kGcStride;
+    for (int i = 0; i < kGcStride - 1; ++i) {
+      double g = 0.0;
+      if (i < a)
+        for (int j = a; j < n; ++j)
+          if ((t >> (j - a)) & 1ull) g += umat[(size_t)i * n + j];
+      row[i] = g;
+    }
+    double hh = 0.0;
+    for (int i = a; i < n; ++i) {
+      if (!((t >> (i - a)) & 1ull)) continue;
+      for (int j = i + 1; j < n; ++j)
+        if ((t >> (j - a)) & 1ull) hh += umat[(size_t)i * n + j];
+    }
+    row[kGcStride - 1] = hh;
+  }
 }
 
 // Diagonal -sum_i delta_i bit_i + sum_{i<j} U_ij bit_i bit_j for every index
@@ -413,8 +514,7 @@ __global__ void interaction_diag_kernel(int n, const double* __restrict__ umat, 
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) su[i] = umat[i];
   __syncthreads();
   const uint64_t total = 1ull << n;
-  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < total;
-       b += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < total; b += (uint64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
     for (int i = 0; i < n; ++i) {
       if (!((b >> i) & 1ull)) continue;
@@ -426,8 +526,8 @@ __global__ void interaction_diag_kernel(int n, const double* __restrict__ umat, 
   }
 }
 
-__global__ void zdotc_kernel(const cplx* __restrict__ x, const cplx* __restrict__ y, uint64_t n,
-                             double* part, unsigned* counter, double* result2) {
+__global__ void zdotc_kernel(const cplx* __restrict__ x, const cplx* __restrict__ y, uint64_t n, double* part,
+                             unsigned* counter, double* result2) {
   __shared__ double red[32];
   double re = 0.0, im = 0.0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -438,12 +538,15 @@ __global__ void zdotc_kernel(const cplx* __restrict__ x, const cplx* __restrict_
   double mine[2] = {block_sum<kThreads>(re, red), block_sum<kThreads>(im, red)};
   double tot[2];
   if (!grid_finalize<2, kThreads>(mine, part, counter, tot, red)) return;
-  if (threadIdx.x == 0) { result2[0] = tot[0]; result2[1] = tot[1]; }
+  if (threadIdx.x == 0) {
+    result2[0] = tot[0];
+    result2[1] = tot[1];
+  }
 }
 
 // sum |x - y|^2 (norm_difference, observables.py:137, without cancellation)
-__global__ void diff_norm_kernel(const cplx* __restrict__ x, const cplx* __restrict__ y, uint64_t n,
-                                 double* part, unsigned* counter, double* result) {
+__global__ void diff_norm_kernel(const cplx* __restrict__ x, const cplx* __restrict__ y, uint64_t n, double* part,
+                                 unsigned* counter, double* result) {
   __shared__ double red[32];
   double s = 0.0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -458,16 +561,21 @@ __global__ void diff_norm_kernel(const cplx* __restrict__ x, const cplx* __restr
 }
 
 // w -= alpha v + beta vprev ; result = ||w||^2 (generic-matvec Lanczos, krylov.py:100-105)
-__global__ void lanczos_update_kernel(cplx* __restrict__ w, const cplx* __restrict__ v,
-                                      const cplx* __restrict__ vprev, double alpha, double beta, uint64_t n,
-                                      double* part, unsigned* counter, double* result) {
+__global__ void lanczos_update_kernel(cplx* __restrict__ w, const cplx* __restrict__ v, const cplx* __restrict__ vprev,
+                                      double alpha, double beta, uint64_t n, double* part, unsigned* counter,
+                                      double* result) {
   __shared__ double red[32];
   double nn = 0.0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     cplx a = w[i];
     const cplx b = v[i];
-    a.x -= alpha * b.x; a.y -= alpha * b.y;
-    if (vprev != nullptr) { const cplx c = vprev[i]; a.x -= beta * c.x; a.y -= beta * c.y; }
+    a.x -= alpha * b.x;
+    a.y -= alpha * b.y;
+    if (vprev != nullptr) {
+      const cplx c = vprev[i];
+      a.x -= beta * c.x;
+      a.y -= beta * c.y;
+    }
     w[i] = a;
     nn = fma(a.x, a.x, fma(a.y, a.y, nn));
   }
@@ -506,104 +614,111 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int TB, int KIND>
-cudaError_t launch_pass_tbk(const PassArgs& args, int grid, cudaStream_t st) {
-  constexpr int TILE = 1 << TB;
-  constexpr int NT = TILE < kThreads ? TILE : kThreads;
-  const size_t smem = TILE * sizeof(cplx);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(pass_kernel<TB, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+unsigned flat_grid(uint64_t n, int grid) {
+  if (grid > 0) return (unsigned)grid;
+  uint64_t blocks = (n + kThreads - 1) / kThreads;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  return (unsigned)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+// Launch with grid = min(tiles, SMs x resident CTAs); the occupancy query is done once per kernel.
+template <typename Kernel, typename Args>
+cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, int nt, size_t smem, int* occ_cache,
+                              cudaStream_t st) {
+  if (*occ_cache == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+    if (e != cudaSuccess) return e;
+    *occ_cache = occ > 0 ? occ : 1;
   }
-  pass_kernel<TB, KIND><<<grid, NT, smem, st>>>(args);
+  const uint64_t cap = (uint64_t)num_sms() * (uint64_t)*occ_cache;
+  const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+  kern<<<grid, nt, smem, st>>>(args);
   return cudaGetLastError();
 }
 
+template <int TB, int KIND>
+cudaError_t launch_pass_tbk(const PassArgs& args, cudaStream_t st) {
+  constexpr int NT = pass_threads(TB, KIND);
+  constexpr int STAGES = TB >= 8 ? RSV_STAGES : 2;
+  static int occ = 0;
+  return launch_persistent(pass_kernel<TB, KIND, NT>, args, args.sh.n_tiles, NT, STAGES * (1 << TB) * sizeof(cplx),
+                           &occ, st);
+}
+
 template <int TB>
-cudaError_t launch_pass_tb(const PassArgs& args, int grid, cudaStream_t st) {
+cudaError_t launch_pass_tb(const PassArgs& args, cudaStream_t st) {
   switch (args.kind) {
-    case PASS_FIRST: return launch_pass_tbk<TB, PASS_FIRST>(args, grid, st);
-    case PASS_MID: return launch_pass_tbk<TB, PASS_MID>(args, grid, st);
-    case PASS_LAST_APPLY: return launch_pass_tbk<TB, PASS_LAST_APPLY>(args, grid, st);
-    case PASS_LAST_LANCZOS: return launch_pass_tbk<TB, PASS_LAST_LANCZOS>(args, grid, st);
+    case PASS_FIRST: return launch_pass_tbk<TB, PASS_FIRST>(args, st);
+    case PASS_MID: return launch_pass_tbk<TB, PASS_MID>(args, st);
+    case PASS_LAST_APPLY: return launch_pass_tbk<TB, PASS_LAST_APPLY>(args, st);
+    case PASS_LAST_LANCZOS: return launch_pass_tbk<TB, PASS_LAST_LANCZOS>(args, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int TB>
-cudaError_t launch_combine_tb(const CombineArgs& args, int grid, cudaStream_t st) {
-  constexpr int TILE = 1 << TB;
-  constexpr int NT = TILE < kThreads ? TILE : kThreads;
-  const size_t smem = TILE * sizeof(cplx);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(combine_kernel<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  combine_kernel<TB><<<grid, NT, smem, st>>>(args);
-  return cudaGetLastError();
+cudaError_t launch_combine_tb(const CombineArgs& args, cudaStream_t st) {
+  constexpr int NT = combine_threads(TB);
+  static int occ = 0;
+  return launch_persistent(combine_kernel<TB, NT>, args, args.sh.n_tiles, NT, (1 << TB) * sizeof(cplx), &occ, st);
 }
 
 }  // namespace
 
-int max_pass_grid(int tile_bits) {
-  // 64 KB tiles: 3 resident CTAs per SM
-  const int per_sm = tile_bits >= 12 ? 3 : 4;
-  return num_sms() * per_sm;
-}
-
-int pass_grid(const Shape& sh) {
-  const uint64_t cap = (uint64_t)max_pass_grid(sh.a + sh.g);
-  return (int)(sh.n_tiles < cap ? sh.n_tiles : cap);
-}
-
-cudaError_t launch_pass(const PassArgs& args, int grid, cudaStream_t st) {
-  const int tb = args.sh.a + args.sh.g;
-  switch (tb) {
-    case 1: return launch_pass_tb<1>(args, grid, st);
-    case 2: return launch_pass_tb<2>(args, grid, st);
-    case 3: return launch_pass_tb<3>(args, grid, st);
-    case 4: return launch_pass_tb<4>(args, grid, st);
-    case 5: return launch_pass_tb<5>(args, grid, st);
-    case 6: return launch_pass_tb<6>(args, grid, st);
-    case 7: return launch_pass_tb<7>(args, grid, st);
-    case 8: return launch_pass_tb<8>(args, grid, st);
-    case 9: return launch_pass_tb<9>(args, grid, st);
-    case 10: return launch_pass_tb<10>(args, grid, st);
-    case 11: return launch_pass_tb<11>(args, grid, st);
-    case 12: return launch_pass_tb<12>(args, grid, st);
+cudaError_t launch_pass(const PassArgs& args, cudaStream_t st) {
+  switch (args.sh.a + args.sh.g) {
+    case 1: return launch_pass_tb<1>(args, st);
+    case 2: return launch_pass_tb<2>(args, st);
+    case 3: return launch_pass_tb<3>(args, st);
+    case 4: return launch_pass_tb<4>(args, st);
+    case 5: return launch_pass_tb<5>(args, st);
+    case 6: return launch_pass_tb<6>(args, st);
+    case 7: return launch_pass_tb<7>(args, st);
+    case 8: return launch_pass_tb<8>(args, st);
+    case 9: return launch_pass_tb<9>(args, st);
+    case 10: return launch_pass_tb<10>(args, st);
+    case 11: return launch_pass_tb<11>(args, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_combine(const CombineArgs& args, int grid, cudaStream_t st) {
-  const int tb = args.sh.a + args.sh.g;
-  switch (tb) {
-    case 1: return launch_combine_tb<1>(args, grid, st);
-    case 2: return launch_combine_tb<2>(args, grid, st);
-    case 3: return launch_combine_tb<3>(args, grid, st);
-    case 4: return launch_combine_tb<4>(args, grid, st);
-    case 5: return launch_combine_tb<5>(args, grid, st);
-    case 6: return launch_combine_tb<6>(args, grid, st);
-    case 7: return launch_combine_tb<7>(args, grid, st);
-    case 8: return launch_combine_tb<8>(args, grid, st);
-    case 9: return launch_combine_tb<9>(args, grid, st);
-    case 10: return launch_combine_tb<10>(args, grid, st);
-    case 11: return launch_combine_tb<11>(args, grid, st);
-    case 12: return launch_combine_tb<12>(args, grid, st);
+cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st) {
+  switch (args.sh.a + args.sh.g) {
+    case 1: return launch_combine_tb<1>(args, st);
+    case 2: return launch_combine_tb<2>(args, st);
+    case 3: return launch_combine_tb<3>(args, st);
+    case 4: return launch_combine_tb<4>(args, st);
+    case 5: return launch_combine_tb<5>(args, st);
+    case 6: return launch_combine_tb<6>(args, st);
+    case 7: return launch_combine_tb<7>(args, st);
+    case 8: return launch_combine_tb<8>(args, st);
+    case 9: return launch_combine_tb<9>(args, st);
+    case 10: return launch_combine_tb<10>(args, st);
+    case 11: return launch_combine_tb<11>(args, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_dev_or_null,
-                            const double* delta_host, int with_interaction, double* dl, cudaStream_t st) {
+cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
+                            double* dl, cudaStream_t st) {
   DiagArgs dg{};
   if (delta_host != nullptr)
     for (int i = 0; i < n && i < kMaxQubits; ++i) dg.delta[i] = delta_host[i];
   const int total = 1 << a;
   const int nt = total < 256 ? total : 256;
-  build_dl_kernel<<<(total + nt - 1) / nt, nt, 0, st>>>(a, n, umat, delta_dev_or_null, dg, with_interaction, dl);
+  build_dl_kernel<<<(total + nt - 1) / nt, nt, 0, st>>>(a, n, umat, dg, with_interaction, dl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_table(int a, int n, const double* umat, double* gc, cudaStream_t st) {
+  const uint64_t ntiles = 1ull << (n - a);
+  uint64_t blocks = (ntiles + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  build_tile_table_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, n, umat, ntiles, gc);
   return cudaGetLastError();
 }
 
@@ -620,30 +735,21 @@ cudaError_t launch_interaction_diag(int n, const double* umat, const double* del
   return cudaGetLastError();
 }
 
-static unsigned flat_grid(uint64_t n, int grid) {
-  if (grid > 0) return (unsigned)grid;
-  uint64_t blocks = (n + kThreads - 1) / kThreads;
-  const uint64_t cap = (uint64_t)num_sms() * 8;
-  return (unsigned)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
-}
-
-cudaError_t launch_zdotc(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter,
-                         double* result2, int grid, cudaStream_t st) {
+cudaError_t launch_zdotc(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter, double* result2,
+                         int grid, cudaStream_t st) {
   zdotc_kernel<<<flat_grid(n, grid), kThreads, 0, st>>>(x, y, n, part, counter, result2);
   return cudaGetLastError();
 }
 
-cudaError_t launch_diff_norm(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter,
-                             double* result, int grid, cudaStream_t st) {
+cudaError_t launch_diff_norm(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter, double* result,
+                             int grid, cudaStream_t st) {
   diff_norm_kernel<<<flat_grid(n, grid), kThreads, 0, st>>>(x, y, n, part, counter, result);
   return cudaGetLastError();
 }
 
-cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, double alpha, double beta,
-                                  uint64_t n, double* part, unsigned* counter, double* result, int grid,
-                                  cudaStream_t st) {
-  lanczos_update_kernel<<<flat_grid(n, grid), kThreads, 0, st>>>(w, v, vprev, alpha, beta, n, part, counter,
-                                                                  result);
+cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, double alpha, double beta, uint64_t n,
+                                  double* part, unsigned* counter, double* result, int grid, cudaStream_t st) {
+  lanczos_update_kernel<<<flat_grid(n, grid), kThreads, 0, st>>>(w, v, vprev, alpha, beta, n, part, counter, result);
   return cudaGetLastError();
 }
 
@@ -656,5 +762,7 @@ cudaError_t launch_scale(cplx* y, const cplx* x, double2 a, uint64_t n, int grid
   scale_kernel<<<flat_grid(n, grid), kThreads, 0, st>>>(y, x, a, n);
   return cudaGetLastError();
 }
+
+int max_grid_rows() { return num_sms() * 8; }
 
 }  // namespace rsv

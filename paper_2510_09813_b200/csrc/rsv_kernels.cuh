@@ -37,7 +37,18 @@ constexpr int kMaxQubits = 48;
 constexpr int kMaxFlips = 16;     // flips per pass (tile bits <= 12)
 constexpr int kMaxKrylov = 96;    // vectors in one Krylov combination
 constexpr int kMaxMasks = 128;    // observable masks per combine
-constexpr int kLoBits = 12;       // tile bits (2^12 complex128 = 64 KB)
+constexpr int kLoBits = 11;       // tile bits (2^11 complex128 = 32 KB per buffer)
+constexpr int kGcStride = 12;     // lo-pass tile table row: gc[0..10] + hh
+
+// CTA size per pass kind (host and device agree on it: the flip split depends on it).
+// The first (lo) pass carries no elementwise operand, so it keeps 8 amplitudes per thread
+// (3 register bits); the passes with elementwise operands prefetch them into registers
+// and use 512 threads x 4 amplitudes.
+constexpr int pass_threads(int tb, int kind) {
+  return (1 << tb) < (kind == 0 ? 256 : 512) ? (1 << tb) : (kind == 0 ? 256 : 512);
+}
+constexpr int combine_threads(int tb) { return (1 << tb) < 256 ? (1 << tb) : 256; }
+constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
 // scalar slots (device double array, reset per step)
 constexpr int SC_N0SQ = 0;        // ||psi||^2 of the step's input state
@@ -68,15 +79,17 @@ struct Shape {
 };
 
 struct FlipSet {
-  int count;
+  int count;                // flips through shared memory (tile bit < log2(threads))
   int mask[kMaxFlips];      // tile-local bit masks
   double coef[kMaxFlips];   // Omega_q / 2
+  double rcoef[4];          // register flips: coefficient of tile bit log2(threads) + b (0 = inactive)
 };
 
 struct DiagArgs {
   int mode;                 // DiagMode (only for passes whose tile is [0, a))
   const double* dl;         // 2^a table: lo part of the diagonal (fly: detuning+interaction, vec: detuning)
-  const double* umat;       // n x n interaction matrix (fly)
+  const double* gc;         // per-run tile table [tiles][kGcStride] (fly): lo-hi couplings + hi-hi energy
+  const double* umat;       // n x n interaction matrix
   const double* dvec;       // 2^n precomputed interaction diagonal (vec)
   double delta[kMaxQubits]; // detunings
 };
@@ -109,11 +122,12 @@ struct CombineArgs {
   double* sc; double* part; unsigned* counter;
 };
 
-// host-side launchers (rsv_kernels.cu)
-cudaError_t launch_pass(const PassArgs& args, int grid, cudaStream_t st);
-cudaError_t launch_combine(const CombineArgs& args, int grid, cudaStream_t st);
-cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_dev_or_null,
-                            const double* delta_host, int with_interaction, double* dl, cudaStream_t st);
+// host-side launchers (rsv_kernels.cu); persistent grids sized from the occupancy query
+cudaError_t launch_pass(const PassArgs& args, cudaStream_t st);
+cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st);
+cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
+                            double* dl, cudaStream_t st);
+cudaError_t launch_tile_table(int a, int n, const double* umat, double* gc, cudaStream_t st);
 cudaError_t launch_interaction_diag(int n, const double* umat, const double* delta_host, double* dvec,
                                     cudaStream_t st);
 cudaError_t launch_zdotc(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter,
@@ -125,7 +139,6 @@ cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, dou
                                   cudaStream_t st);
 cudaError_t launch_axpy(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
 cudaError_t launch_scale(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
-int max_pass_grid(int tile_bits);
-int pass_grid(const Shape& sh);
+int max_grid_rows();   // upper bound on the grid of any kernel writing partial rows
 
 }  // namespace rsv
