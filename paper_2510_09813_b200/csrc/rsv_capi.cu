@@ -202,14 +202,18 @@ void build_plan(rsv_context* c) {
   c->plan.push_back(lo);
   const int rem = n - alo;
   if (rem <= 0) return;
-  const int gmax = rsv::kLoBits - 2;   // hi tile = 2^(TB-g) contiguous x 2^g strided, runs >= 64 B
+  // hi groups of <= 9 bits keep >= 3 contiguous low bits in a 2^12 tile (runs >= 128 B);
+  // balanced sizes, the largest first, the smallest last (it also runs the q-sweep).
+  const int gmax = rsv::kLoBits - 3;
   const int ng = (rem + gmax - 1) / gmax;
   std::vector<int> sizes;
   for (int i = 0; i < ng; ++i) sizes.push_back(rem / ng + (i < rem % ng ? 1 : 0));   // descending
   int top = n;
   for (int s : sizes) {
     PassPlan p;
-    const int a = rsv::kLoBits - s;
+    // contiguous run 2^a with a <= log2(pass threads): the register bits of a thread are then
+    // all group bits, so its amplitudes sit at one uniform stride (pass_kernel, S)
+    const int a = std::min(rsv::kLoBits - s, rsv::ilog2(rsv::pass_threads(rsv::kLoBits)));
     p.sh = rsv::Shape{n, a, top - s, s, 1ull << (n - a - s)};
     p.q0 = top - s;
     p.nq = s;
@@ -219,13 +223,12 @@ void build_plan(rsv_context* c) {
   }
 }
 
-rsv::FlipSet flips_for(const PassPlan& p, const double* omegas, int kind) {
+rsv::FlipSet flips_for(const PassPlan& p, const double* omegas, int nthreads) {
   // Tile bits below log2(threads per CTA) are flipped through shared memory, the
   // ones above are register permutations inside a thread (pass_kernel, RegBits).
   rsv::FlipSet f{};
   f.count = 0;
-  const int tb = p.sh.a + p.sh.g;
-  const int lt = rsv::ilog2(rsv::pass_threads(tb, kind));
+  const int lt = rsv::ilog2(nthreads);
   for (int q = p.q0; q < p.q0 + p.nq; ++q) {
     const double cq = 0.5 * omegas[q];
     if (cq == 0.0) continue;   // zero drives are skipped, as in _kernels.py:19
@@ -256,10 +259,11 @@ rsv::DiagArgs diag_for(const rsv_context* c, const PassPlan& p, const double* de
 
 int ensure_dl(rsv_context* c, const double* deltas) {
   const int alo = c->plan[0].sh.a;
-  std::vector<double> key(deltas, deltas + alo);
+  std::vector<double> key(deltas, deltas + c->n);
   if (c->dl_valid && key == c->dl_key) return RSV_OK;
-  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, deltas, c->diag_mode == RSV_DIAG_FLY ? 1 : 0, c->d_dl,
-                                c->st));
+  const bool fly = c->diag_mode == RSV_DIAG_FLY;
+  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, deltas, fly ? 1 : 0, c->d_dl, c->st));
+  CUDA_TRY(rsv::launch_tile_base(alo, c->n, fly ? 1 : 0, deltas, c->d_gc, c->st));
   c->dl_key = key;
   c->dl_valid = true;
   return RSV_OK;
@@ -315,7 +319,7 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
   A.sh = last.sh;
   A.qsweep = q_omegas != nullptr ? 1 : 0;
   if (A.qsweep) {
-    A.fl = flips_for(last, q_omegas, rsv::PASS_FIRST);   // combine CTAs use the FIRST-pass thread count
+    A.fl = flips_for(last, q_omegas, rsv::combine_threads(last.sh.a + last.sh.g));
     A.dg = diag_for(c, last, q_deltas);
     if (last.lo) {
       int rc = ensure_dl(c, q_deltas);
@@ -369,7 +373,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     const bool last = pi + 1 == np;
     A.kind = last ? rsv::PASS_LAST_LANCZOS : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
-    A.fl = flips_for(p, omegas, A.kind);
+    A.fl = flips_for(p, omegas, rsv::pass_threads(p.sh.a + p.sh.g));
     A.dg = diag_for(c, p, deltas);
     A.x = slot(c, j);
     A.x_scale_slot = rsv::SC_SG + j;
@@ -377,15 +381,16 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     A.sc = c->d_sc;
     A.part = c->d_part;
     A.counter = c->d_counter;
-    if (!last) {
-      A.uin = pi == 0 ? nullptr : work(c);
-      A.out = work(c);
+    // elementwise operand: -beta' s_{j-1} joins in the first pass, the partial sum u in the others
+    if (pi == 0) {
+      A.ein = j > 0 ? slot(c, j - 1) : nullptr;
+      A.ein_is_prev = 1;
     } else {
-      A.uin = np > 1 ? work(c) : nullptr;
-      A.out = slot(c, j + 1);
-      A.prev = j > 0 ? slot(c, j - 1) : nullptr;
-      A.qsweep = 1;
+      A.ein = work(c);
+      A.ein_is_prev = 0;
     }
+    A.out = last ? slot(c, j + 1) : work(c);
+    A.qsweep = last ? 1 : 0;
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
@@ -553,6 +558,7 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_dl, sizeof(double) << rsv::kLoBits);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_gc, sizeof(double) * rsv::kGcStride * gc_rows);
+
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_pin, sizeof(double) * rsv::SC_SIZE);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->obs_event, cudaEventDisableTiming);
   if (e == cudaSuccess)
@@ -649,7 +655,7 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     rsv::PassArgs A{};
     A.kind = pi + 1 == np ? rsv::PASS_LAST_APPLY : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
-    A.fl = flips_for(p, omegas, A.kind);
+    A.fl = flips_for(p, omegas, rsv::pass_threads(p.sh.a + p.sh.g));
     A.dg = diag_for(c, p, deltas);
     A.x = reinterpret_cast<const cplx*>(psi);
     A.x_scale_slot = rsv::SC_ONE;
@@ -658,11 +664,8 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     A.part = c->d_part;
     A.counter = c->d_counter;
     A.out = reinterpret_cast<cplx*>(out);
-    if (pi + 1 == np) {
-      A.uin = np > 1 ? reinterpret_cast<const cplx*>(out) : nullptr;
-    } else {
-      A.uin = pi == 0 ? nullptr : reinterpret_cast<const cplx*>(out);
-    }
+    A.ein = pi == 0 ? nullptr : reinterpret_cast<const cplx*>(out);
+    A.ein_is_prev = 0;
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);

@@ -4,6 +4,9 @@
 #ifndef RSV_STAGES
 #define RSV_STAGES 2
 #endif
+#ifndef RSV_L2_PREFETCH
+#define RSV_L2_PREFETCH 1
+#endif
 
 namespace rsv {
 
@@ -115,23 +118,22 @@ template <int NT, int EPT>
 struct DiagRow {
   double d[EPT];
 
-  __device__ __forceinline__ void setup(const DiagArgs& dg, const Shape& sh, uint64_t t, int tid) {
+  // row: shared copy of [gc[t][0..11], hh[t], tb[t]] (see pass_kernel), or nullptr to read global
+  __device__ __forceinline__ void setup(const DiagArgs& dg, const Shape& sh, uint64_t t, int tid,
+                                        const double* row) {
     constexpr int LT = Log2<NT>::value;
     constexpr int RB = RegBits<EPT>::value;
-    const int a = sh.a, n = sh.n;
-    double base = 0.0;
-    for (int j = a; j < n; ++j)
-      if ((t >> (j - a)) & 1ull) base -= dg.delta[j];
+    const int a = sh.a;
+    const double base = row ? row[13] : __ldg(dg.gc + t * kGcStride + 13);   // tb[t] = hh[t] - sum_{j>=a} delta_j bit_j(t)
     double cross_t = 0.0;
     double gy[RB > 0 ? RB : 1];
     if (dg.mode == DIAG_FLY) {
-      const double* g = dg.gc + t * kGcStride;
-      base += __ldg(g + kGcStride - 1);   // hh[t] stored in the last column
+      const double* g = row ? row : dg.gc + t * kGcStride;
       #pragma unroll
       for (int b = 0; b < LT; ++b)
-        if (b < a && ((tid >> b) & 1)) cross_t += __ldg(g + b);
+        if (b < a && ((tid >> b) & 1)) cross_t += g[b];
       #pragma unroll
-      for (int b = 0; b < RB; ++b) gy[b] = (LT + b < a) ? __ldg(g + LT + b) : 0.0;
+      for (int b = 0; b < RB; ++b) gy[b] = (LT + b < a) ? g[LT + b] : 0.0;
     } else {
       #pragma unroll
       for (int b = 0; b < RB; ++b) gy[b] = 0.0;
@@ -153,7 +155,11 @@ struct DiagRow {
 // operands (uin, prev) are prefetched into registers at the top of each iteration. Thread
 // tid owns tile elements e_i = tid + i*NT: flips on tile bits >= log2(NT) are register
 // permutations, the others one conflict-free 16-byte shared load per element.
-template <int TB, int KIND, int NT>
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+template <int TB, int KIND, int NT, bool DIAG>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
@@ -167,60 +173,74 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
   const int tid = threadIdx.x;
   const double* sc = A.sc;
   const double xs = sc[A.x_scale_slot];
-  const bool has_diag = A.dg.mode != DIAG_NONE;
-  double alpha = 0.0, bprev = 0.0;
-  if (LANCZOS) {
-    alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
-    if (A.prev != nullptr && A.j > 0) bprev = sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1];
-  }
+  double alpha = 0.0;
+  if (LANCZOS) alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
+  const bool has_e = A.ein != nullptr;
+  const double ecoef = A.ein_is_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 1.0;
+  // coefficients pre-scaled by the operand scale (v = xs * x)
   double rc[RB > 0 ? RB : 1];
   #pragma unroll
-  for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b];
-  const bool has_u = KIND != PASS_FIRST && A.uin != nullptr;
-  const bool has_prev = LANCZOS && bprev != 0.0;
+  for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
+  const double axs = alpha * xs;
   double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
-  uint64_t off[EPT];
-  #pragma unroll
-  for (int i = 0; i < EPT; ++i) off[i] = elem_offset(A.sh, i * NT);
+  // element i of a thread sits at index(t, tid) + i*S: the plan keeps the i*NT bits either all
+  // contiguous (lo tile) or all in the strided group (hi tiles, a <= log2 NT)
+  const uint64_t S = elem_offset(A.sh, NT);
 
   const uint64_t ntiles = A.sh.n_tiles;
   const uint64_t G = gridDim.x;
+  // shared layout: x ring [STAGES][TILE] | elementwise-operand buffer [TILE] | tile-table rows [STAGES][16]
+  cplx* ubuf = sbuf + STAGES * TILE;
+  double* rows = reinterpret_cast<double*>(sbuf + (STAGES + 1) * TILE);
+  auto issue_x = [&](uint64_t tt, int st_idx) {
+    const cplx* src = A.x + tile_index(A.sh, tt, tid);
+    cplx* dst = sbuf + st_idx * TILE + tid;
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) cp_async16(dst + i * NT, src + i * S);
+    if (DIAG)
+      for (int k = tid; k < kGcStride / 2; k += NT) cp_async16(rows + st_idx * 16 + 2 * k, A.dg.gc + tt * kGcStride + 2 * k);
+  };
   #pragma unroll
   for (int s0 = 0; s0 < STAGES - 1; ++s0) {
     const uint64_t tp = blockIdx.x + (uint64_t)s0 * G;
-    if (tp < ntiles) {
-      const cplx* src = A.x + tile_index(A.sh, tp, tid);
-      cplx* dst = sbuf + s0 * TILE + tid;
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) cp_async16(dst + i * NT, src + off[i]);
-    }
+    if (tp < ntiles) issue_x(tp, s0);
     cp_async_commit();
   }
   int stage = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += G, stage = (stage + 1 == STAGES ? 0 : stage + 1)) {
     const uint64_t g0 = tile_index(A.sh, t, tid);
-    const uint64_t tn = t + (uint64_t)(STAGES - 1) * G;
-    if (tn < ntiles) {
-      const cplx* src = A.x + tile_index(A.sh, tn, tid);
-      cplx* dst = sbuf + (stage == 0 ? STAGES - 1 : stage - 1) * TILE + tid;
+    // group A_t: this tile's elementwise operand u (each thread copies and later reads only its own
+    // amplitudes, so no barrier is needed around ubuf)
+    if (has_e) {
       #pragma unroll
-      for (int i = 0; i < EPT; ++i) cp_async16(dst + i * NT, src + off[i]);
+      for (int i = 0; i < EPT; ++i) cp_async16(ubuf + tid + i * NT, A.ein + g0 + i * S);
     }
     cp_async_commit();
-    cplx uv[EPT], pv[EPT];
-    if (has_u) {
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) uv[i] = ld_stream(A.uin + g0 + off[i]);
+    // group B_t: the x tile (and tile-table row) one ring ahead
+    const uint64_t tn = t + (uint64_t)(STAGES - 1) * G;
+    if (tn < ntiles) issue_x(tn, stage == 0 ? STAGES - 1 : stage - 1);
+    cp_async_commit();
+#if RSV_L2_PREFETCH
+    if ((tid & 7) == 0) {
+      const uint64_t t1 = t + G, t2 = t + (uint64_t)STAGES * G;
+      if (t1 < ntiles && has_e) {
+        const uint64_t g1 = tile_index(A.sh, t1, tid);
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) prefetch_l2(A.ein + g1 + i * S);
+      }
+      if (t2 < ntiles) {
+        const uint64_t g2 = tile_index(A.sh, t2, tid);
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) prefetch_l2(A.x + g2 + i * S);
+      }
     }
-    if (has_prev) {
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) pv[i] = ld_stream(A.prev + g0 + off[i]);
-    }
-    DiagRow<NT, EPT> dr;
-    if (has_diag) dr.setup(A.dg, A.sh, t, tid);
-    cp_async_wait<STAGES - 1>();
+#endif
+    // x(t) was group B_{t-1}: at most A_t and B_t may still be in flight
+    cp_async_wait<STAGES>();
     __syncthreads();
-    cplx* s = sbuf + stage * TILE;
+    const cplx* s = sbuf + stage * TILE;
+    DiagRow<NT, EPT> dr;
+    if (DIAG) dr.setup(A.dg, A.sh, t, tid, rows + stage * 16);
 
     cplx xv[EPT], ac[EPT];
     #pragma unroll
@@ -237,73 +257,74 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
       }
     }
     for (int f = 0; f < A.fl.count; ++f) {
-      const int m = A.fl.mask[f];
-      const double c = A.fl.coef[f];
+      const cplx* ps = s + (tid ^ A.fl.mask[f]);   // partner of element i is ps[i*NT]
+      const double c = A.fl.coef[f] * xs;
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        const cplx p = s[(tid + i * NT) ^ m];
+        const cplx p = ps[i * NT];
         ac[i].x = fma(c, p.x, ac[i].x);
         ac[i].y = fma(c, p.y, ac[i].y);
       }
     }
-    if (has_diag) {
+    if (DIAG) {
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         double d = dr.d[i];
-        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + off[i]);
+        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+        d *= xs;
         ac[i].x = fma(d, xv[i].x, ac[i].x);
         ac[i].y = fma(d, xv[i].y, ac[i].y);
       }
     }
+    if (has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may still be in flight
+    cplx* po = A.out + g0;
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-      double cr = ac[i].x * xs, ci = ac[i].y * xs;   // this pass's operator applied to v = xs * x
-      acc_a = fma(xs * xv[i].x, cr, fma(xs * xv[i].y, ci, acc_a));
-      if (has_u) {
-        cr += uv[i].x;
-        ci += uv[i].y;
+      double cr = ac[i].x, ci = ac[i].y;   // this pass's operator applied to v = xs * x
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
+      if (has_e) {
+        const cplx u = ubuf[tid + i * NT];
+        cr = fma(ecoef, u.x, cr);
+        ci = fma(ecoef, u.y, ci);
       }
       if (LANCZOS) {
-        cr = fma(-alpha * xs, xv[i].x, cr);
-        ci = fma(-alpha * xs, xv[i].y, ci);
-        if (has_prev) {
-          cr = fma(-bprev, pv[i].x, cr);
-          ci = fma(-bprev, pv[i].y, ci);
-        }
+        cr = fma(-axs, xv[i].x, cr);
+        ci = fma(-axs, xv[i].y, ci);
         acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
       ac[i] = make_double2(cr, ci);
-      st_stream(A.out + g0 + off[i], ac[i]);
+      st_stream(po + i * S, ac[i]);
     }
 
     if (LANCZOS && A.qsweep) {
       // q-sweep: <w | A_this w> while w is on chip (this pass's share of alpha_{j+1})
       __syncthreads();
+      cplx* sw = sbuf + stage * TILE;
       #pragma unroll
-      for (int i = 0; i < EPT; ++i) s[tid + i * NT] = ac[i];
+      for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
       __syncthreads();
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         double hr = 0.0, hi = 0.0;
         #pragma unroll
         for (int b = 0; b < RB; ++b) {
-          hr = fma(rc[b], ac[i ^ (1 << b)].x, hr);
-          hi = fma(rc[b], ac[i ^ (1 << b)].y, hi);
+          hr = fma(A.fl.rcoef[b], ac[i ^ (1 << b)].x, hr);
+          hi = fma(A.fl.rcoef[b], ac[i ^ (1 << b)].y, hi);
         }
-        if (has_diag) {
+        if (DIAG) {
           double d = dr.d[i];
-          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + off[i]);
+          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
           hr = fma(d, ac[i].x, hr);
           hi = fma(d, ac[i].y, hi);
         }
         acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
       }
       for (int f = 0; f < A.fl.count; ++f) {
-        const int m = A.fl.mask[f];
+        const cplx* ps = sw + (tid ^ A.fl.mask[f]);
         const double c = A.fl.coef[f];
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-          const cplx p = s[(tid + i * NT) ^ m];
+          const cplx p = ps[i * NT];
           acc_q = fma(c, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
         }
       }
@@ -311,6 +332,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
     __syncthreads();
   }
   cp_async_wait<0>();
+  acc_a *= xs;
 
   if (KIND == PASS_LAST_APPLY) return;
   double mine[3];
@@ -379,7 +401,7 @@ __global__ void __launch_bounds__(NT, 2) combine_kernel(const __grid_constant__ 
     }
     if (A.qsweep) {
       DiagRow<NT, EPT> dr;
-      if (has_diag) dr.setup(A.dg, A.sh, t, tid);
+      if (has_diag) dr.setup(A.dg, A.sh, t, tid, nullptr);
       #pragma unroll
       for (int i = 0; i < EPT; ++i) s[tid + i * NT] = wv[i];
       __syncthreads();
@@ -482,14 +504,14 @@ __global__ void build_dl_kernel(int a, int n, const double* __restrict__ umat, D
   dl[e] = v;
 }
 
-// Per-run tile table of the lo pass: gc[t][i] = sum_{j>=a} U_ij bit_j(t) (i < a) and, in the
-// last column, hh[t] = sum_{a<=i<j} U_ij bit_i(t) bit_j(t).
+// Per-run tile table of the lo pass, row t: gc[t][i] = sum_{j>=a} U_ij bit_j(t) (i < a, cols 0..11),
+// hh[t] = sum_{a<=i<j} U_ij bit_i(t) bit_j(t) (col 12); col 13 (tb) is filled per step.
 __global__ void build_tile_table_kernel(int a, int n, const double* __restrict__ umat, uint64_t ntiles,
                                         double* __restrict__ gc) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
        t += (uint64_t)gridDim.x * blockDim.x) {
     double* row = gc + t * kGcStride;
-    for (int i = 0; i < kGcStride - 1; ++i) {
+    for (int i = 0; i < 12; ++i) {
       double g = 0.0;
       if (i < a)
         for (int j = a; j < n; ++j)
@@ -502,7 +524,19 @@ __global__ void build_tile_table_kernel(int a, int n, const double* __restrict__
       for (int j = i + 1; j < n; ++j)
         if ((t >> (j - a)) & 1ull) hh += umat[(size_t)i * n + j];
     }
-    row[kGcStride - 1] = hh;
+    row[12] = hh;
+    row[13] = hh;
+  }
+}
+
+// Per-step tile base (col 13): tb[t] = hh[t] (fly) - sum_{j>=a} delta_j bit_j(t).
+__global__ void build_tile_base_kernel(int a, int n, int fly, DiagArgs dg, uint64_t ntiles, double* __restrict__ gc) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    double v = fly ? gc[t * kGcStride + 12] : 0.0;
+    for (int j = a; j < n; ++j)
+      if ((t >> (j - a)) & 1ull) v -= dg.delta[j];
+    gc[t * kGcStride + 13] = v;
   }
 }
 
@@ -639,13 +673,26 @@ cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, in
   return cudaGetLastError();
 }
 
-template <int TB, int KIND>
-cudaError_t launch_pass_tbk(const PassArgs& args, cudaStream_t st) {
-  constexpr int NT = pass_threads(TB, KIND);
+template <int TB, int KIND, bool DIAG>
+cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
+  constexpr int NT = pass_threads(TB);
   constexpr int STAGES = TB >= 8 ? RSV_STAGES : 2;
   static int occ = 0;
-  return launch_persistent(pass_kernel<TB, KIND, NT>, args, args.sh.n_tiles, NT, STAGES * (1 << TB) * sizeof(cplx),
-                           &occ, st);
+  constexpr size_t smem = (STAGES + 1) * (1 << TB) * sizeof(cplx) + STAGES * 16 * sizeof(double);
+  return launch_persistent(pass_kernel<TB, KIND, NT, DIAG>, args, args.sh.n_tiles, NT, smem, &occ, st);
+}
+
+template <int TB, int KIND>
+cudaError_t launch_pass_tbk(const PassArgs& args, cudaStream_t st) {
+  // the diagonal lives in the lo pass only: the middle passes never carry it
+  if constexpr (KIND == PASS_MID) {
+    return launch_pass_tbkd<TB, KIND, false>(args, st);
+  } else if constexpr (KIND == PASS_FIRST) {
+    return launch_pass_tbkd<TB, KIND, true>(args, st);   // the first pass is always the lo pass
+  } else {
+    if (args.dg.mode != DIAG_NONE) return launch_pass_tbkd<TB, KIND, true>(args, st);
+    return launch_pass_tbkd<TB, KIND, false>(args, st);
+  }
 }
 
 template <int TB>
@@ -681,6 +728,7 @@ cudaError_t launch_pass(const PassArgs& args, cudaStream_t st) {
     case 9: return launch_pass_tb<9>(args, st);
     case 10: return launch_pass_tb<10>(args, st);
     case 11: return launch_pass_tb<11>(args, st);
+    case 12: return launch_pass_tb<12>(args, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -698,6 +746,7 @@ cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st) {
     case 9: return launch_combine_tb<9>(args, st);
     case 10: return launch_combine_tb<10>(args, st);
     case 11: return launch_combine_tb<11>(args, st);
+    case 12: return launch_combine_tb<12>(args, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -719,6 +768,17 @@ cudaError_t launch_tile_table(int a, int n, const double* umat, double* gc, cuda
   const uint64_t cap = (uint64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   build_tile_table_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, n, umat, ntiles, gc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_base(int a, int n, int fly, const double* delta_host, double* gc, cudaStream_t st) {
+  const uint64_t ntiles = 1ull << (n - a);
+  uint64_t blocks = (ntiles + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  DiagArgs dg{};
+  for (int i = 0; i < n && i < kMaxQubits; ++i) dg.delta[i] = delta_host[i];
+  build_tile_base_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, n, fly, dg, ntiles, gc);
   return cudaGetLastError();
 }
 

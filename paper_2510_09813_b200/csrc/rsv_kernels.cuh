@@ -37,16 +37,15 @@ constexpr int kMaxQubits = 48;
 constexpr int kMaxFlips = 16;     // flips per pass (tile bits <= 12)
 constexpr int kMaxKrylov = 96;    // vectors in one Krylov combination
 constexpr int kMaxMasks = 128;    // observable masks per combine
-constexpr int kLoBits = 11;       // tile bits (2^11 complex128 = 32 KB per buffer)
-constexpr int kGcStride = 12;     // lo-pass tile table row: gc[0..10] + hh
+constexpr int kLoBits = 12;       // tile bits: 2^12 complex128 = 64 KB per tile buffer
+constexpr int kGcStride = 14;     // lo-pass tile table row: gc[0..11], hh, tb (112 B, cp.async-able)
 
-// CTA size per pass kind (host and device agree on it: the flip split depends on it).
-// The first (lo) pass carries no elementwise operand, so it keeps 8 amplitudes per thread
-// (3 register bits); the passes with elementwise operands prefetch them into registers
-// and use 512 threads x 4 amplitudes.
-constexpr int pass_threads(int tb, int kind) {
-  return (1 << tb) < (kind == 0 ? 256 : 512) ? (1 << tb) : (kind == 0 ? 256 : 512);
-}
+// CTA size of the pass kernels (host and device agree on it: the flip split depends on it).
+// 512 threads x 8 amplitudes: the top 3 tile bits are register bits.
+#ifndef RSV_PASS_THREADS
+#define RSV_PASS_THREADS 512
+#endif
+constexpr int pass_threads(int tb) { return (1 << tb) < RSV_PASS_THREADS ? (1 << tb) : RSV_PASS_THREADS; }
 constexpr int combine_threads(int tb) { return (1 << tb) < 256 ? (1 << tb) : 256; }
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
@@ -65,7 +64,7 @@ enum PassKind : int {
   PASS_FIRST = 0,         // out = A x            ; ap[j]  = <x|A x>
   PASS_MID = 1,           // out = uin + A x      ; ap[j] += <x|A x>
   PASS_LAST_APPLY = 2,    // out = uin + A x       (plain H.psi)
-  PASS_LAST_LANCZOS = 3,  // out = uin + A x - alpha x - beta' prev ; beta, q_{j+1}
+  PASS_LAST_LANCZOS = 3,  // out = uin + A x - alpha x ; beta, q_{j+1} (-beta' prev enters in the first pass)
 };
 
 enum DiagMode : int { DIAG_NONE = 0, DIAG_FLY = 1, DIAG_VEC = 2 };
@@ -100,9 +99,11 @@ struct PassArgs {
   DiagArgs dg;
   int kind;
   const cplx* x; int x_scale_slot;      // operand s_j, v_j = sc[slot] * s_j
-  const cplx* uin;                      // partial sum from previous passes (may be null)
+  const cplx* ein;                      // elementwise operand (may be null): the partial sum u of the
+                                        // previous passes (coefficient 1) or, in the first pass of a
+                                        // Lanczos iteration, s_{j-1} (coefficient -beta_{j-1} sigma_{j-1})
+  int ein_is_prev;
   cplx* out;
-  const cplx* prev;                     // s_{j-1} (LAST_LANCZOS, j > 0)
   int j;                                // Lanczos iteration
   int qsweep;                           // LAST_LANCZOS: compute q_{j+1}
   double* sc; double* part; unsigned* counter;
@@ -128,6 +129,7 @@ cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st);
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
                             double* dl, cudaStream_t st);
 cudaError_t launch_tile_table(int a, int n, const double* umat, double* gc, cudaStream_t st);
+cudaError_t launch_tile_base(int a, int n, int fly, const double* delta_host, double* gc, cudaStream_t st);
 cudaError_t launch_interaction_diag(int n, const double* umat, const double* delta_host, double* dvec,
                                     cudaStream_t st);
 cudaError_t launch_zdotc(const cplx* x, const cplx* y, uint64_t n, double* part, unsigned* counter,
