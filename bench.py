@@ -222,14 +222,21 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ our arm
 def alg_bytes_per_launch(family, n, k_avg, diag):
+    """Algorithmic HBM bytes of one launch of a kernel family ('Roofline accounting').
+
+    lo   : read s_j (16 B) + s_{j-1} (16 B, all but the first iteration of a step) + write u (16 B)
+           (+ 8 B of precomputed diagonal for diag='vec')
+    mid  : read s_j + u, write u            (48 B)
+    last : read s_j + u, write s_{j+1}      (48 B)
+    combine : read the k basis vectors, write psi ((k + 1) x 16 B)
+    """
     amp = 2 ** n
     if family == "lo":
-        return (32 + (8 if diag == "vec" else 0)) * amp          # read x (+diag), write u
-    if family == "mid":
-        return 48 * amp                                          # read x, u; write u
-    if family == "last":
-        return 64 * amp                                          # read x, u, s_{j-1}; write w_j
-    return (k_avg + 1) * 16 * amp                                # combine: read k basis vectors, write psi
+        prev_frac = (k_avg - 1.0) / k_avg if k_avg > 0 else 0.0
+        return (32 + 16 * prev_frac + (8 if diag == "vec" else 0)) * amp
+    if family in ("mid", "last"):
+        return 48 * amp
+    return (k_avg + 1) * 16 * amp
 
 
 def run_ours(args):

@@ -140,8 +140,7 @@ std::vector<zc> tridiag_exp_e1(const std::vector<double>& a, const std::vector<d
 
 struct PassPlan {
   rsv::Shape sh;
-  int q0;     // first qubit of the group
-  int nq;     // qubits in the group
+  std::vector<int> qubits;   // qubits whose flips this pass applies (all inside its tile)
   bool lo;    // lo tile (bits [0, a)) carries the diagonal
 };
 
@@ -190,36 +189,52 @@ cplx* slot(const rsv_context* c, int logical_index) {
 }
 cplx* work(const rsv_context* c) { return slot(c, (int)c->logical.size() - 1); }
 
+// Pass plan: the lo pass (tile = bits [0, 12), carries the diagonal) and hi passes over groups
+// of <= 9 high bits (tile = 2^a contiguous x 2^g strided rows). Smaller groups sit at the top
+// of the index so the most strided passes get the longest contiguous runs; the lowest group
+// runs last (it also carries the q-sweep). When a middle pass exists, the lowest qubits'
+// flips move from the lo pass (the heaviest: 12 flips + diagonal) to the first middle pass,
+// whose tile contains those bits too.
+constexpr int kDelegateLow = 3;
+
 void build_plan(rsv_context* c) {
   const int n = c->n;
   c->plan.clear();
   const int alo = std::min(n, rsv::kLoBits);
   PassPlan lo;
   lo.sh = rsv::Shape{n, alo, alo, 0, 1ull << (n - alo)};
-  lo.q0 = 0;
-  lo.nq = alo;
+  for (int q = 0; q < alo; ++q) lo.qubits.push_back(q);
   lo.lo = true;
   c->plan.push_back(lo);
   const int rem = n - alo;
   if (rem <= 0) return;
-  // hi groups of <= 9 bits keep >= 3 contiguous low bits in a 2^12 tile (runs >= 128 B);
-  // balanced sizes, the largest first, the smallest last (it also runs the q-sweep).
   const int gmax = rsv::kLoBits - 3;
   const int ng = (rem + gmax - 1) / gmax;
-  std::vector<int> sizes;
-  for (int i = 0; i < ng; ++i) sizes.push_back(rem / ng + (i < rem % ng ? 1 : 0));   // descending
+  std::vector<int> sizes;   // ascending: the top (most strided) groups are the smallest
+  for (int i = 0; i < ng; ++i) sizes.push_back(rem / ng + (i >= ng - rem % ng ? 1 : 0));
+  std::vector<PassPlan> hi;
   int top = n;
+  const int lt = rsv::ilog2(rsv::pass_threads(rsv::kLoBits));
   for (int s : sizes) {
     PassPlan p;
     // contiguous run 2^a with a <= log2(pass threads): the register bits of a thread are then
     // all group bits, so its amplitudes sit at one uniform stride (pass_kernel, S)
-    const int a = std::min(rsv::kLoBits - s, rsv::ilog2(rsv::pass_threads(rsv::kLoBits)));
+    const int a = std::min(rsv::kLoBits - s, lt);
     p.sh = rsv::Shape{n, a, top - s, s, 1ull << (n - a - s)};
-    p.q0 = top - s;
-    p.nq = s;
+    for (int q = top - s; q < top; ++q) p.qubits.push_back(q);
     p.lo = false;
-    c->plan.push_back(p);
+    hi.push_back(p);
     top -= s;
+  }
+  // execution order: lo, the top groups, last = the lowest group (least strided: its q-sweep and
+  // its write of the next Krylov vector stream best there)
+  for (size_t i = 0; i + 1 < hi.size(); ++i) c->plan.push_back(hi[i]);
+  c->plan.push_back(hi.back());
+  if (c->plan.size() >= 3 && c->plan[1].sh.a >= kDelegateLow && alo > kDelegateLow) {
+    PassPlan& l = c->plan[0];
+    PassPlan& m = c->plan[1];
+    l.qubits.erase(l.qubits.begin(), l.qubits.begin() + kDelegateLow);
+    for (int q = 0; q < kDelegateLow; ++q) m.qubits.push_back(q);
   }
 }
 
@@ -229,10 +244,10 @@ rsv::FlipSet flips_for(const PassPlan& p, const double* omegas, int nthreads) {
   rsv::FlipSet f{};
   f.count = 0;
   const int lt = rsv::ilog2(nthreads);
-  for (int q = p.q0; q < p.q0 + p.nq; ++q) {
+  for (int q : p.qubits) {
     const double cq = 0.5 * omegas[q];
     if (cq == 0.0) continue;   // zero drives are skipped, as in _kernels.py:19
-    const int local = p.lo ? q : p.sh.a + (q - p.sh.p);
+    const int local = (p.lo || q < p.sh.a) ? q : p.sh.a + (q - p.sh.p);
     if (local >= lt) {
       f.rcoef[local - lt] = cq;
     } else {
@@ -272,7 +287,8 @@ int ensure_dl(rsv_context* c, const double* deltas) {
 // Key of everything the prepared q_0 depends on: last-pass drives (+ detunings if it holds the diagonal).
 std::vector<double> prep_key_for(const rsv_context* c, const double* omegas, const double* deltas) {
   const PassPlan& last = c->plan.back();
-  std::vector<double> k(omegas + last.q0, omegas + last.q0 + last.nq);
+  std::vector<double> k;
+  for (int q : last.qubits) k.push_back(omegas[q]);
   if (last.lo) k.insert(k.end(), deltas, deltas + c->n);
   return k;
 }

@@ -7,6 +7,10 @@
 #ifndef RSV_L2_PREFETCH
 #define RSV_L2_PREFETCH 1
 #endif
+// elementwise operand staged through shared memory (cp.async) or prefetched into registers
+#ifndef RSV_EIN_REGS
+#define RSV_EIN_REGS 0
+#endif
 
 namespace rsv {
 
@@ -211,9 +215,13 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
     const uint64_t g0 = tile_index(A.sh, t, tid);
     // group A_t: this tile's elementwise operand u (each thread copies and later reads only its own
     // amplitudes, so no barrier is needed around ubuf)
+    cplx ev[EPT];
     if (has_e) {
       #pragma unroll
-      for (int i = 0; i < EPT; ++i) cp_async16(ubuf + tid + i * NT, A.ein + g0 + i * S);
+      for (int i = 0; i < EPT; ++i) {
+        if (RSV_EIN_REGS) ev[i] = ld_stream(A.ein + g0 + i * S);
+        else cp_async16(ubuf + tid + i * NT, A.ein + g0 + i * S);
+      }
     }
     cp_async_commit();
     // group B_t: the x tile (and tile-table row) one ring ahead
@@ -276,14 +284,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
         ac[i].y = fma(d, xv[i].y, ac[i].y);
       }
     }
-    if (has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may still be in flight
+    if (!RSV_EIN_REGS && has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may be in flight
     cplx* po = A.out + g0;
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;   // this pass's operator applied to v = xs * x
       acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
-        const cplx u = ubuf[tid + i * NT];
+        const cplx u = RSV_EIN_REGS ? ev[i] : ubuf[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
         ci = fma(ecoef, u.y, ci);
       }

@@ -26,7 +26,7 @@ for k in range(3, 3 + steps):
     mv += r.matvecs
 prof = eng.profile()
 amp = 2 ** n
-alg = {"lo": 32 * amp, "mid": 48 * amp, "last": 64 * amp}
+alg = {"lo": 48 * amp, "mid": 48 * amp, "last": 48 * amp}   # x + elementwise operand + out
 out = {"lib": os.environ.get("RSV_LIB", "default"), "n": n, "matvecs": mv}
 for f, v in prof.items():
     if v["launches"] and f in alg:
