@@ -1,0 +1,213 @@
+"""State sharding by the top log2(P) qubits across P processes (one GPU each).
+
+North-star row (e): an N-qubit state is split into P = 2^k contiguous shards of 2^(N-k)
+amplitudes; rank r holds the indices whose top k bits equal r. Then
+
+* every flip on a local qubit (i < N-k) and every diagonal term are shard-local: the local
+  passes run unchanged with *effective* detunings
+      delta_eff_i = delta_i - sum_{g global, bit_g(r)=1} U_ig
+  and a constant per-rank energy offset
+      E_r = -sum_{g set} delta_g + sum_{g<g' set} U_gg';
+* a flip on a global qubit g is the elementwise exchange
+      y_r += (Omega_g / 2) * psi_{r ^ 2^(g-N+k)}
+  with the partner rank (NCCL send/recv or P2P loads over NVLink);
+* the Lanczos scalars (alpha, beta, norms) and observables are all-reduced.
+
+This module holds that host-side logic. It is backend-agnostic: a ``LocalOps`` object supplies
+the shard-local arithmetic (the rsv C ABI on a GPU; the CPU tests plug a numpy restatement) and a
+``Comm`` object the exchange/all-reduce (torch.distributed: NCCL on GPUs, gloo in the CPU tests).
+The reference algorithm of rydsim/krylov.py:67-125 (with its full re-orthogonalisation) runs on
+top, so a sharded run is checked against the unsharded oracle.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ValidationError
+
+NS_TO_US = 1e-3
+_BREAKDOWN_RTOL = 1e-14
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    n_qubits: int
+    world_size: int
+    rank: int
+
+    def __post_init__(self):
+        p = self.world_size
+        if p < 1 or p & (p - 1):
+            raise ValidationError(f"world size {p} is not a power of two")
+        if not 0 <= self.rank < p:
+            raise ValidationError(f"rank {self.rank} outside [0, {p})")
+        if self.n_global >= self.n_qubits:
+            raise ValidationError(f"{p} shards need more than {self.n_global} qubits")
+
+    @property
+    def n_global(self) -> int:
+        return int(math.log2(self.world_size))
+
+    @property
+    def n_local(self) -> int:
+        return self.n_qubits - self.n_global
+
+    @property
+    def global_qubits(self):
+        return list(range(self.n_local, self.n_qubits))
+
+    def global_bit(self, q: int) -> int:
+        return (self.rank >> (q - self.n_local)) & 1
+
+    def partner(self, q: int) -> int:
+        """Rank holding the amplitudes with qubit q (global) flipped."""
+        return self.rank ^ (1 << (q - self.n_local))
+
+    def local_slice(self):
+        size = 1 << self.n_local
+        return slice(self.rank * size, (self.rank + 1) * size)
+
+    def local_parameters(self, omegas, deltas, u):
+        """(local omegas, effective local deltas, local U, energy offset, global flips).
+
+        global flips: list of (qubit, Omega_q / 2, partner rank) for nonzero drives.
+        """
+        omegas = np.asarray(omegas, dtype=float)
+        deltas = np.asarray(deltas, dtype=float)
+        u = np.asarray(u, dtype=float)
+        nl = self.n_local
+        set_g = [g for g in self.global_qubits if self.global_bit(g)]
+        d_eff = deltas[:nl].copy()
+        for g in set_g:
+            d_eff -= u[:nl, g]
+        offset = -sum(deltas[g] for g in set_g)
+        for a_i, g in enumerate(set_g):
+            for h in set_g[a_i + 1:]:
+                offset += u[g, h]
+        flips = [(g, 0.5 * omegas[g], self.partner(g)) for g in self.global_qubits if omegas[g] != 0.0]
+        return omegas[:nl].copy(), d_eff, u[:nl, :nl].copy(), float(offset), flips
+
+
+class ShardedOperator:
+    """y = H psi for a sharded psi: local passes + offset + partner exchanges."""
+
+    def __init__(self, plan: ShardPlan, local_ops, comm, omegas, deltas, u):
+        self.plan = plan
+        self.ops = local_ops
+        self.comm = comm
+        self.om, self.de, self.u, self.offset, self.flips = plan.local_parameters(omegas, deltas, u)
+
+    def __call__(self, x):
+        y = self.ops.apply_local(self.om, self.de, self.u, x)
+        if self.offset != 0.0:
+            self.ops.axpy(y, x, self.offset)
+        for _q, coef, partner in self.flips:
+            peer = self.comm.exchange(x, partner)
+            self.ops.axpy(y, peer, coef)
+        return y
+
+
+def tridiag_exp_e1(alphas, betas, tau):
+    k = len(alphas)
+    if k == 1:
+        return np.array([np.exp(-1j * tau * alphas[0])])
+    t = np.diag(np.asarray(alphas, dtype=float))
+    idx = np.arange(k - 1)
+    t[idx, idx + 1] = betas
+    t[idx + 1, idx] = betas
+    lam, z = np.linalg.eigh(t)
+    return z @ (np.exp(-1j * tau * lam) * z[0, :])
+
+
+def sharded_expm_multiply(op: ShardedOperator, psi, dt_ns, tolerance=1e-10, max_krylov_dim=100,
+                          norm_epsilon=1e-14):
+    """krylov.py:67-125 over shards: every inner product is an all-reduce."""
+    ops, comm = op.ops, op.comm
+
+    def dot(a, b):
+        return comm.allreduce_complex(ops.vdot(a, b))
+
+    norm_in = math.sqrt(max(0.0, dot(psi, psi).real))
+    if norm_in <= norm_epsilon:
+        return ops.copy(psi), 0, True, 0.0
+    if dt_ns == 0.0:
+        return ops.copy(psi), 1, True, 0.0
+    tau = dt_ns * NS_TO_US
+    basis = [ops.scaled(psi, 1.0 / norm_in)]
+    alphas, betas = [], []
+    converged = False
+    residual = math.inf
+    while True:
+        w = op(basis[-1])
+        a = dot(basis[-1], w).real
+        alphas.append(a)
+        ops.axpy(w, basis[-1], -a)
+        if betas:
+            ops.axpy(w, basis[-2], -betas[-1])
+        for v in basis:
+            ops.axpy(w, v, -dot(v, w))
+        b = math.sqrt(max(0.0, dot(w, w).real))
+        y = tridiag_exp_e1(alphas, betas, tau)
+        residual = b * abs(y[-1])
+        scale = max(1.0, max(abs(x) for x in alphas), max(betas, default=0.0))
+        if residual <= tolerance or b <= _BREAKDOWN_RTOL * scale:
+            converged = True
+            break
+        if len(alphas) >= max_krylov_dim:
+            break
+        betas.append(b)
+        basis.append(ops.scaled(w, 1.0 / b))
+    out = ops.zeros_like(psi)
+    for coef, v in zip(y, basis):
+        ops.axpy(out, v, complex(coef) * norm_in)
+    return out, len(alphas), converged, float(residual)
+
+
+def sharded_occupations(plan: ShardPlan, local_ops, comm, psi):
+    """<n_q> for all N qubits: local bits reduce on the shard, global bits are rank constants."""
+    local_occ, local_norm = local_ops.occupations_unnormalised(psi)
+    tot = comm.allreduce_real(np.concatenate([local_occ, [local_norm]]))
+    occ_local = tot[:-1] / tot[-1]
+    glob = np.array([plan.global_bit(g) * local_norm for g in plan.global_qubits])
+    glob = comm.allreduce_real(glob) / tot[-1]
+    return np.concatenate([occ_local, glob])
+
+
+class TorchComm:
+    """Exchange / all-reduce over torch.distributed (NCCL on GPUs, gloo in CPU tests)."""
+
+    def __init__(self, dist, device=None):
+        self.dist = dist
+        self.device = device
+
+    def exchange(self, x, partner):
+        import torch
+
+        send = torch.as_tensor(x)
+        recv = torch.empty_like(send)
+        rank = self.dist.get_rank()
+        # deadlock-free pairwise exchange: the lower rank sends first
+        if rank < partner:
+            self.dist.send(send, partner)
+            self.dist.recv(recv, partner)
+        else:
+            self.dist.recv(recv, partner)
+            self.dist.send(send, partner)
+        return recv if not isinstance(x, np.ndarray) else recv.numpy()
+
+    def allreduce_real(self, arr):
+        import torch
+
+        t = torch.as_tensor(np.asarray(arr, dtype=np.float64).copy())
+        if self.device is not None:
+            t = t.to(self.device)
+        self.dist.all_reduce(t)
+        return t.cpu().numpy()
+
+    def allreduce_complex(self, z):
+        r = self.allreduce_real([z.real, z.imag])
+        return complex(r[0], r[1])
