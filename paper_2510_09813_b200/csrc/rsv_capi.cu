@@ -195,7 +195,13 @@ cplx* work(const rsv_context* c) { return slot(c, (int)c->logical.size() - 1); }
 // runs last (it also carries the q-sweep). When a middle pass exists, the lowest qubits'
 // flips move from the lo pass (the heaviest: 12 flips + diagonal) to the first middle pass,
 // whose tile contains those bits too.
-constexpr int kDelegateLow = 3;
+#ifndef RSV_DELEGATE_LOW
+#define RSV_DELEGATE_LOW 3
+#endif
+#ifndef RSV_LAST_TOP
+#define RSV_LAST_TOP 1
+#endif
+constexpr int kDelegateLow = RSV_DELEGATE_LOW;
 
 void build_plan(rsv_context* c) {
   const int n = c->n;
@@ -228,9 +234,14 @@ void build_plan(rsv_context* c) {
   }
   // execution order: lo, the top groups, last = the lowest group (least strided: its q-sweep and
   // its write of the next Krylov vector stream best there)
+#if RSV_LAST_TOP
+  for (size_t i = hi.size() - 1; i >= 1; --i) c->plan.push_back(hi[i]);
+  c->plan.push_back(hi[0]);
+#else
   for (size_t i = 0; i + 1 < hi.size(); ++i) c->plan.push_back(hi[i]);
   c->plan.push_back(hi.back());
-  if (c->plan.size() >= 3 && c->plan[1].sh.a >= kDelegateLow && alo > kDelegateLow) {
+#endif
+  if (kDelegateLow > 0 && c->plan.size() >= 3 && c->plan[1].sh.a >= kDelegateLow && alo > kDelegateLow) {
     PassPlan& l = c->plan[0];
     PassPlan& m = c->plan[1];
     l.qubits.erase(l.qubits.begin(), l.qubits.begin() + kDelegateLow);
@@ -418,7 +429,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
 int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, double dt_ns, double tol,
                    int kmax, double norm_eps, const double* next_omegas, const double* next_deltas,
                    int observe, rsv_krylov_report* rep, int depth) {
-  if (depth > 24) return fail(RSV_ERR_NOT_CONVERGED, "sub-step recursion too deep");
+  if (depth > 64) return fail(RSV_ERR_NOT_CONVERGED, "sub-step recursion too deep");
   if (!c->prep_valid || c->prep_key != prep_key_for(c, omegas, deltas)) {
     int rc = prepare(c, omegas, deltas);
     if (rc) return rc;
@@ -476,20 +487,28 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
   }
 
   double tau_used = tau;
-  int nsub = 1;
+  double dt_rest = 0.0;
   if (!converged && k >= cap && k < kmax) {
-    // Split exp(-i tau H) = exp(-i tau/2^s H)^(2^s): the same Krylov basis gives the
-    // first sub-step; the rest are fresh Lanczos runs on the advanced state.
-    for (int s = 1; s <= 20; ++s) {
-      const double ts = tau / double(1 << s);
-      std::vector<zc> ys = tridiag_exp_e1(alphas, betas, ts, false);
-      if (beta * std::abs(ys.back()) <= tol) {
-        tau_used = ts;
-        nsub = 1 << s;
-        residual = beta * std::abs(ys.back());
-        converged = true;
-        break;
+    // HBM cap reached: exp(-i tau H) = exp(-i (tau - tau') H) exp(-i tau' H) exactly. The basis
+    // already built gives the largest tau' whose a-posteriori estimate meets the tolerance
+    // (bisection on the same T_k); the rest of the step is a fresh Lanczos run.
+    double lo = 0.0, hi = 1.0, r_lo = 0.0;
+    for (int it = 0; it < 48; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      const std::vector<zc> ys = tridiag_exp_e1(alphas, betas, mid * tau, false);
+      const double r = beta * std::abs(ys.back());
+      if (r <= tol) {
+        lo = mid;
+        r_lo = r;
+      } else {
+        hi = mid;
       }
+    }
+    if (lo > 0.0) {
+      tau_used = lo * tau;
+      dt_rest = dt_ns * (1.0 - lo);
+      residual = r_lo;
+      converged = true;
     }
   }
   y = tridiag_exp_e1(alphas, betas, tau_used, true);
@@ -503,7 +522,7 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
     const double sigma = i == 0 ? 1.0 / n0 : 1.0 / betas[i - 1];
     coef[i] = y[i] * (n0 * sigma);
   }
-  const bool more = nsub > 1;
+  const bool more = dt_rest > 0.0;
   const double* qo = more ? omegas : next_omegas;
   const double* qd = more ? deltas : next_deltas;
   rc = run_combine(c, k, coef, work(c), qo, qd, (!more && observe) ? 1 : 0);
@@ -516,14 +535,10 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
     c->prep_valid = false;
   }
   if (more) {
-    rep->substeps += nsub - 1;
-    const double dts = dt_ns / nsub;
-    for (int r = 1; r < nsub; ++r) {
-      const bool final_sub = r + 1 == nsub;
-      rc = expm_step_impl(c, omegas, deltas, dts, tol, kmax, norm_eps, final_sub ? next_omegas : omegas,
-                          final_sub ? next_deltas : deltas, final_sub ? observe : 0, rep, depth + 1);
-      if (rc) return rc;
-    }
+    rep->substeps += 1;
+    rc = expm_step_impl(c, omegas, deltas, dt_rest, tol, kmax, norm_eps, next_omegas, next_deltas, observe, rep,
+                        depth + 1);
+    if (rc) return rc;
   }
   return RSV_OK;
 }

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
     if (has_e) {
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        if (RSV_EIN_REGS) ev[i] = ld_stream(A.ein + g0 + i * S);
+        if (RSV_EIN_REGS && KIND != PASS_FIRST) ev[i] = ld_stream(A.ein + g0 + i * S);
         else cp_async16(ubuf + tid + i * NT, A.ein + g0 + i * S);
       }
     }
@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
     if (tn < ntiles) issue_x(tn, stage == 0 ? STAGES - 1 : stage - 1);
     cp_async_commit();
 #if RSV_L2_PREFETCH
-    if ((tid & 7) == 0) {
+    // only for the contiguous lo tile: on strided tiles the extra LSU traffic costs more than it saves
+    if (DIAG && (tid & 7) == 0) {
       const uint64_t t1 = t + G, t2 = t + (uint64_t)STAGES * G;
       if (t1 < ntiles && has_e) {
         const uint64_t g1 = tile_index(A.sh, t1, tid);
@@ -284,14 +285,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
         ac[i].y = fma(d, xv[i].y, ac[i].y);
       }
     }
-    if (!RSV_EIN_REGS && has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may be in flight
+    if (!(RSV_EIN_REGS && KIND != PASS_FIRST) && has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may be in flight
     cplx* po = A.out + g0;
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;   // this pass's operator applied to v = xs * x
       acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
-        const cplx u = RSV_EIN_REGS ? ev[i] : ubuf[tid + i * NT];
+        const cplx u = (RSV_EIN_REGS && KIND != PASS_FIRST) ? ev[i] : ubuf[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
         ci = fma(ecoef, u.y, ci);
       }
@@ -311,13 +312,15 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
       #pragma unroll
       for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
       __syncthreads();
+      // <w|X_k|w> = 2 Re sum_{bit k of b = 0} conj(w_b) w_{b^k}: each pair is visited once
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         double hr = 0.0, hi = 0.0;
         #pragma unroll
         for (int b = 0; b < RB; ++b) {
-          hr = fma(A.fl.rcoef[b], ac[i ^ (1 << b)].x, hr);
-          hi = fma(A.fl.rcoef[b], ac[i ^ (1 << b)].y, hi);
+          if ((i >> b) & 1) continue;
+          hr = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].x, hr);
+          hi = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].y, hi);
         }
         if (DIAG) {
           double d = dr.d[i];
@@ -328,12 +331,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
         acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
       }
       for (int f = 0; f < A.fl.count; ++f) {
-        const cplx* ps = sw + (tid ^ A.fl.mask[f]);
-        const double c = A.fl.coef[f];
+        const int m = A.fl.mask[f];
+        if (tid & m) continue;   // partner visits the pair (whole warps skip for mask >= 32)
+        const cplx* ps = sw + (tid ^ m);
+        const double c2 = 2.0 * A.fl.coef[f];
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           const cplx p = ps[i * NT];
-          acc_q = fma(c, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
+          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
         }
       }
     }
