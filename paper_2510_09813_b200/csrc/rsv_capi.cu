@@ -425,11 +425,13 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
   return RSV_OK;
 }
 
-// One exact step of length dt on the resident state (may recurse into sub-steps).
-int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, double dt_ns, double tol,
-                   int kmax, double norm_eps, const double* next_omegas, const double* next_deltas,
-                   int observe, rsv_krylov_report* rep, int depth) {
-  if (depth > 64) return fail(RSV_ERR_NOT_CONVERGED, "sub-step recursion too deep");
+// One Lanczos run on the resident state for a time step of dt_rest (<= the requested step).
+// Returns the fraction of dt_rest actually advanced (1 when converged on the full step, < 1
+// when the Krylov basis hit the HBM cap and the step was split).
+int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, double dt_rest, double tol, int kmax,
+                double norm_eps, const double* q_omegas, const double* q_deltas, bool last_run, int observe,
+                rsv_krylov_report* rep, bool first_run, double* advanced, bool* zero_vector) {
+  *zero_vector = false;
   if (!c->prep_valid || c->prep_key != prep_key_for(c, omegas, deltas)) {
     int rc = prepare(c, omegas, deltas);
     if (rc) return rc;
@@ -438,7 +440,7 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
   if (rc) return rc;
   CUDA_TRY(cudaMemsetAsync(c->d_sc + rsv::SC_AP, 0, sizeof(double) * 128, c->st));
 
-  const double tau = dt_ns * kNsToUs;
+  const double tau = dt_rest * kNsToUs;
   const int cap = kcap(c);
   std::vector<double> alphas, betas;
   std::vector<zc> y;
@@ -460,14 +462,15 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
     prof_collect(c);
     if (j == 0) {
       n0 = std::sqrt(std::max(0.0, c->h_pin[rsv::SC_N0SQ]));
-      rep->norm_in = n0;
+      if (first_run) {
+        rep->norm_in = n0;
+        rep->alpha0 = c->h_pin[rsv::SC_AL];
+      }
       if (n0 <= norm_eps) {   // krylov.py:83-84: zero vector returned unchanged
-        rep->iterations = std::max(rep->iterations, 0);
-        rep->converged = 1;
-        rep->residual = 0.0;
+        *zero_vector = true;
+        *advanced = 1.0;
         return RSV_OK;
       }
-      rep->alpha0 = c->h_pin[rsv::SC_AL];
     }
     alphas.push_back(c->h_pin[rsv::SC_AL + j]);
     beta = c->h_pin[rsv::SC_BE + j];
@@ -486,12 +489,11 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
     betas.push_back(beta);
   }
 
-  double tau_used = tau;
-  double dt_rest = 0.0;
+  double frac = 1.0;
   if (!converged && k >= cap && k < kmax) {
     // HBM cap reached: exp(-i tau H) = exp(-i (tau - tau') H) exp(-i tau' H) exactly. The basis
     // already built gives the largest tau' whose a-posteriori estimate meets the tolerance
-    // (bisection on the same T_k); the rest of the step is a fresh Lanczos run.
+    // (bisection on the same T_k); the caller continues with the rest of the step.
     double lo = 0.0, hi = 1.0, r_lo = 0.0;
     for (int it = 0; it < 48; ++it) {
       const double mid = 0.5 * (lo + hi);
@@ -505,16 +507,15 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
       }
     }
     if (lo > 0.0) {
-      tau_used = lo * tau;
-      dt_rest = dt_ns * (1.0 - lo);
+      frac = lo;
       residual = r_lo;
       converged = true;
     }
   }
-  y = tridiag_exp_e1(alphas, betas, tau_used, true);
+  y = tridiag_exp_e1(alphas, betas, frac * tau, true);
   rep->iterations = std::max(rep->iterations, k);
-  rep->residual = std::max(depth == 0 ? 0.0 : rep->residual, residual);
-  rep->converged = (depth == 0 ? 1 : rep->converged) && converged;
+  rep->residual = std::max(rep->residual, residual);
+  if (!converged) rep->converged = 0;
 
   // psi_new = n0 * sum_i y_i v_i, v_0 = s_0/n0, v_i = s_i / beta_{i-1}
   std::vector<zc> coef(k);
@@ -522,10 +523,10 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
     const double sigma = i == 0 ? 1.0 / n0 : 1.0 / betas[i - 1];
     coef[i] = y[i] * (n0 * sigma);
   }
-  const bool more = dt_rest > 0.0;
-  const double* qo = more ? omegas : next_omegas;
-  const double* qd = more ? deltas : next_deltas;
-  rc = run_combine(c, k, coef, work(c), qo, qd, (!more && observe) ? 1 : 0);
+  const bool more = frac < 1.0;
+  const double* qo = more ? omegas : q_omegas;
+  const double* qd = more ? deltas : q_deltas;
+  rc = run_combine(c, k, coef, work(c), qo, qd, (!more && last_run && observe) ? 1 : 0);
   if (rc) return rc;
   std::swap(c->logical[0], c->logical[c->logical.size() - 1]);
   if (qo != nullptr) {
@@ -534,13 +535,30 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
   } else {
     c->prep_valid = false;
   }
-  if (more) {
-    rep->substeps += 1;
-    rc = expm_step_impl(c, omegas, deltas, dt_rest, tol, kmax, norm_eps, next_omegas, next_deltas, observe, rep,
-                        depth + 1);
-    if (rc) return rc;
-  }
+  *advanced = frac;
   return RSV_OK;
+}
+
+// One exact step of length dt on the resident state, split into as many Lanczos runs as the
+// resident Krylov basis requires.
+int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, double dt_ns, double tol,
+                   int kmax, double norm_eps, const double* next_omegas, const double* next_deltas,
+                   int observe, rsv_krylov_report* rep) {
+  rep->converged = 1;
+  rep->residual = 0.0;
+  double remaining = dt_ns;
+  for (int run = 0;; ++run) {
+    if (run > 100000) return fail(RSV_ERR_NOT_CONVERGED, "step split into more than 1e5 Krylov runs");
+    double frac = 1.0;
+    bool zero = false;
+    int rc = lanczos_run(c, omegas, deltas, remaining, tol, kmax, norm_eps, next_omegas, next_deltas, true,
+                         observe, rep, run == 0, &frac, &zero);
+    if (rc) return rc;
+    if (zero) return RSV_OK;
+    if (!rep->converged || frac >= 1.0) return RSV_OK;
+    remaining *= (1.0 - frac);
+    rep->substeps += 1;
+  }
 }
 
 }  // namespace
@@ -727,7 +745,7 @@ int rsv_expm_step(rsv_context* c, const double* omegas, const double* deltas, do
     return RSV_OK;
   }
   return expm_step_impl(c, omegas, deltas, dt_ns, tolerance, max_krylov_dim, norm_epsilon, next_omegas,
-                        next_deltas, observe, report, 0);
+                        next_deltas, observe, report);
 }
 
 int rsv_set_observables(rsv_context* c, const uint64_t* masks, int nmask) {
