@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
     if (has_e) {
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        if (RSV_EIN_REGS && KIND != PASS_FIRST) ev[i] = ld_stream(A.ein + g0 + i * S);
+        if (RSV_EIN_REGS && KIND == PASS_MID) ev[i] = ld_stream(A.ein + g0 + i * S);
         else cp_async16(ubuf + tid + i * NT, A.ein + g0 + i * S);
       }
     }
@@ -285,14 +285,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
         ac[i].y = fma(d, xv[i].y, ac[i].y);
       }
     }
-    if (!(RSV_EIN_REGS && KIND != PASS_FIRST) && has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may be in flight
+    if (!(RSV_EIN_REGS && KIND == PASS_MID) && has_e) cp_async_wait<1>();   // A_t (this tile's operand) done; B_t may be in flight
     cplx* po = A.out + g0;
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;   // this pass's operator applied to v = xs * x
       acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
-        const cplx u = (RSV_EIN_REGS && KIND != PASS_FIRST) ? ev[i] : ubuf[tid + i * NT];
+        const cplx u = (RSV_EIN_REGS && KIND == PASS_MID) ? ev[i] : ubuf[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
         ci = fma(ecoef, u.y, ci);
       }
