@@ -19,6 +19,10 @@
 #include "rsv.h"
 #include "rsv_kernels.cuh"
 
+#ifndef RSV_TENSOR_MAPS
+#define RSV_TENSOR_MAPS 1   // 5-D TMA descriptors for the strided tiles (0: per-warp bulk runs)
+#endif
+
 using rsv::cplx;
 typedef std::complex<double> zc;
 
@@ -136,6 +140,51 @@ std::vector<zc> tridiag_exp_e1(const std::vector<double>& a, const std::vector<d
     y[ids[q]] = acc;
   }
   return y;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 5-D view of a 2^n complex128 vector whose box is one strided tile of shape sh:
+// [2^(a+1) doubles | 2^(p-a) mid tiles | 2^g1 group rows | 2^g2 group rows | 2^(n-p-g) hi tiles]
+bool encode_tile_map(CUtensorMap* m, const void* base, const rsv::Shape& sh) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr || sh.a > 7 || base == nullptr) return false;
+  const int g1 = std::min(sh.g, 8), g2 = sh.g - g1, hb = sh.n - sh.p - sh.g;
+  cuuint64_t dim[5] = {2ull << sh.a, 1ull << (sh.p - sh.a), 1ull << g1, 1ull << g2, 1ull << hb};
+  cuuint64_t stride[4] = {16ull << sh.a, 16ull << sh.p, 16ull << (sh.p + g1), 16ull << (sh.p + sh.g)};
+  cuuint32_t box[5] = {2u << sh.a, 1u, 1u << g1, 1u << g2, 1u};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dim, stride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Choose the tile-load mode of a pass and encode its TMA descriptors.
+void set_tile_load(rsv::PassArgs& A) {
+  const rsv::Shape& sh = A.sh;
+  if (sh.g == 0) {
+    A.load = rsv::LOAD_CONTIG;
+    return;
+  }
+  A.load = rsv::LOAD_RUNS;
+  if (RSV_TENSOR_MAPS && sh.a <= 7 && encode_tile_map(&A.tm_x, A.x, sh) &&
+      (A.ein == nullptr || encode_tile_map(&A.tm_e, A.ein, sh)))
+    A.load = rsv::LOAD_TENSOR;
 }
 
 struct PassPlan {
@@ -418,6 +467,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     }
     A.out = last ? slot(c, j + 1) : work(c);
     A.qsweep = last ? 1 : 0;
+    set_tile_load(A);
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
@@ -715,6 +765,7 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     A.out = reinterpret_cast<cplx*>(out);
     A.ein = pi == 0 ? nullptr : reinterpret_cast<const cplx*>(out);
     A.ein_is_prev = 0;
+    set_tile_load(A);
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);

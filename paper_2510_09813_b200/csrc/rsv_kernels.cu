@@ -8,6 +8,14 @@
 #define RSV_L2_PREFETCH 1
 #endif
 // elementwise operand staged through shared memory (cp.async) or prefetched into registers
+// issue the next x tile before (1, needs an end-of-tile barrier) or after (0) the tile wait
+#ifndef RSV_EARLY_ISSUE
+#define RSV_EARLY_ISSUE 0
+#endif
+// bulk-async (TMA) data movement in the pass kernels (0: per-thread cp.async)
+#ifndef RSV_TMA
+#define RSV_TMA 1
+#endif
 #ifndef RSV_EIN_REGS
 #define RSV_EIN_REGS 0
 #endif
@@ -25,6 +33,41 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// ---- mbarrier + bulk (TMA) copies
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+        "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 __device__ __forceinline__ cplx ld_stream(const cplx* p) {
   // streaming 128-bit load (evict-first). Coherent path on purpose: the
@@ -224,10 +267,12 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
       }
     }
     cp_async_commit();
+#if RSV_EARLY_ISSUE
     // group B_t: the x tile (and tile-table row) one ring ahead
     const uint64_t tn = t + (uint64_t)(STAGES - 1) * G;
     if (tn < ntiles) issue_x(tn, stage == 0 ? STAGES - 1 : stage - 1);
     cp_async_commit();
+#endif
 #if RSV_L2_PREFETCH
     // only for the contiguous lo tile: on strided tiles the extra LSU traffic costs more than it saves
     if (DIAG && (tid & 7) == 0) {
@@ -244,9 +289,22 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
       }
     }
 #endif
+#if RSV_EARLY_ISSUE
     // x(t) was group B_{t-1}: at most A_t and B_t may still be in flight
     cp_async_wait<STAGES>();
     __syncthreads();
+#else
+    // x(t) was group B_{t-1}: only A_t may still be in flight
+    cp_async_wait<1>();
+    __syncthreads();
+    {
+      // group B_t: every thread is past its reads of the buffer tile t+G overwrites (it belonged to
+      // tile t-G, processed before this barrier), so no end-of-tile barrier is needed
+      const uint64_t tn = t + (uint64_t)(STAGES - 1) * G;
+      if (tn < ntiles) issue_x(tn, stage == 0 ? STAGES - 1 : stage - 1);
+      cp_async_commit();
+    }
+#endif
     const cplx* s = sbuf + stage * TILE;
     DiagRow<NT, EPT> dr;
     if (DIAG) dr.setup(A.dg, A.sh, t, tid, rows + stage * 16);
@@ -342,7 +400,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
         }
       }
     }
+#if RSV_EARLY_ISSUE
     __syncthreads();
+#endif
   }
   cp_async_wait<0>();
   acc_a *= xs;
@@ -361,6 +421,227 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
   } else if (KIND == PASS_MID) {
     scw[SC_AP + A.j] += tot[0];
   } else {  // LAST_LANCZOS
+    const double nrm2 = tot[1];
+    const double beta = sqrt(nrm2);
+    scw[SC_AL + A.j] = alpha;
+    scw[SC_BE + A.j] = beta;
+    scw[SC_SG + A.j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
+    scw[SC_Q + A.j + 1] = nrm2 > 0.0 ? tot[2] / nrm2 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- bit-group pass, TMA version
+// Same arithmetic as pass_kernel; the data movement is bulk-async (TMA engine) instead of
+// per-thread cp.async: each warp copies its own amplitudes' contiguous runs (min(2^a, 32)
+// amplitudes) with cp.async.bulk, completion is tracked by mbarriers (expected-transaction
+// bytes), so the LSU/MIO queues only carry the shared-memory partner loads and the stores.
+//   x ring : 2 stages, tile t+G is requested right after the tile-t barrier
+//   e buf  : this tile's elementwise operand, requested after the same barrier, awaited
+//            just before the epilogue
+template <int TB, int KIND, int NT, bool DIAG>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const __grid_constant__ PassArgs A) {
+  constexpr int TILE = 1 << TB;
+  constexpr int EPT = TILE / NT;
+  constexpr int RB = RegBits<EPT>::value;
+  constexpr bool LANCZOS = KIND == PASS_LAST_LANCZOS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // TMA tensor destinations need 128-byte alignment; the dynamic window starts after the
+  // static shared variables, so align by hand (the launch adds 128 bytes of slack)
+  unsigned char* smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  cplx* xbuf = reinterpret_cast<cplx*>(smem_al);             // [2][TILE]
+  cplx* ebuf = xbuf + 2 * TILE;                               // [TILE]
+  double* rows = reinterpret_cast<double*>(ebuf + TILE);     // [2][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 32);   // xbar[0], xbar[1], ebar
+  __shared__ double red[32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* sc = A.sc;
+  const double xs = sc[A.x_scale_slot];
+  double alpha = 0.0;
+  if (LANCZOS) alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
+  const bool has_e = A.ein != nullptr;
+  const double ecoef = A.ein_is_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 1.0;
+  double rc[RB > 0 ? RB : 1];
+  #pragma unroll
+  for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
+  const double axs = alpha * xs;
+  double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
+  const uint64_t S = elem_offset(A.sh, NT);
+  const uint64_t ntiles = A.sh.n_tiles;
+  const uint64_t G = gridDim.x;
+
+  // copy geometry: a warp owns tile elements [32 w + NT i, +32) for i < EPT, made of
+  // runs of R amplitudes contiguous in global memory (R = 2^a, capped at the warp's 32)
+  const int R = (1 << A.sh.a) < 32 ? (1 << A.sh.a) : (NT < 32 ? NT : 32);
+  const int RUNS = (NT < 32 ? NT : 32) / R;   // runs per warp per i
+  const unsigned tile_bytes = TILE * sizeof(cplx) + (DIAG ? 112u : 0u);
+  auto issue = [&](const cplx* base, const CUtensorMap* map, uint64_t tt, cplx* dst, uint64_t* bar) {
+    if (A.load == LOAD_CONTIG) {
+      if (tid == 0) bulk_g2s(dst, base + tile_index(A.sh, tt, 0), TILE * sizeof(cplx), bar);
+      return;
+    }
+    if (A.load == LOAD_TENSOR) {
+      if (tid == 0) {
+        const int m = A.sh.p - A.sh.a;
+        tma_load_5d(dst, map, 0, (int)(tt & ((1ull << m) - 1ull)), 0, 0, (int)(tt >> m), bar);
+      }
+      return;
+    }
+    // lane k < RUNS copies run k of every i-chunk of this warp
+    if (lane < RUNS) {
+      const uint32_t e0 = (uint32_t)(warp * 32 + lane * R);
+      const cplx* src = base + tile_index(A.sh, tt, e0);
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) bulk_g2s(dst + e0 + i * NT, src + i * S, R * sizeof(cplx), bar);
+    }
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  unsigned xphase[2] = {0u, 0u}, ephase = 0u;
+  // prologue: tile blockIdx.x into stage 0
+  if (blockIdx.x < ntiles) {
+    if (tid == 0) mbar_arrive_expect_tx(&bars[0], tile_bytes);
+    __syncthreads();
+    issue(A.x, &A.tm_x, blockIdx.x, xbuf, &bars[0]);
+    if (DIAG && tid == 0) bulk_g2s(rows, A.dg.gc + blockIdx.x * kGcStride, 112, &bars[0]);
+  }
+  int stage = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += G, stage ^= 1) {
+    const uint64_t g0 = tile_index(A.sh, t, tid);
+    const uint64_t tn = t + G;
+    // arm the barriers before the tile barrier so every copy is issued after its expect_tx
+    if (tid == 0) {
+      if (tn < ntiles) mbar_arrive_expect_tx(&bars[stage ^ 1], tile_bytes);
+      if (has_e) mbar_arrive_expect_tx(&bars[2], TILE * sizeof(cplx));
+    }
+    mbar_wait(&bars[stage], xphase[stage]);
+    xphase[stage] ^= 1u;
+    __syncthreads();   // everyone is done with tile t-G: its x buffer and the e buffer are free
+    if (tn < ntiles) {
+      issue(A.x, &A.tm_x, tn, xbuf + (stage ^ 1) * TILE, &bars[stage ^ 1]);
+      if (DIAG && tid == 0) bulk_g2s(rows + (stage ^ 1) * 16, A.dg.gc + tn * kGcStride, 112, &bars[stage ^ 1]);
+    }
+    if (has_e) issue(A.ein, &A.tm_e, t, ebuf, &bars[2]);
+    const cplx* s = xbuf + stage * TILE;
+    DiagRow<NT, EPT> dr;
+    if (DIAG) dr.setup(A.dg, A.sh, t, tid, rows + stage * 16);
+
+    cplx xv[EPT], ac[EPT];
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      xv[i] = s[tid + i * NT];
+      ac[i] = make_double2(0.0, 0.0);
+    }
+    #pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        ac[i].x = fma(rc[b], xv[i ^ (1 << b)].x, ac[i].x);
+        ac[i].y = fma(rc[b], xv[i ^ (1 << b)].y, ac[i].y);
+      }
+    }
+    for (int f = 0; f < A.fl.count; ++f) {
+      const cplx* ps = s + (tid ^ A.fl.mask[f]);
+      const double c = A.fl.coef[f] * xs;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const cplx p = ps[i * NT];
+        ac[i].x = fma(c, p.x, ac[i].x);
+        ac[i].y = fma(c, p.y, ac[i].y);
+      }
+    }
+    if (DIAG) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        double d = dr.d[i];
+        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+        d *= xs;
+        ac[i].x = fma(d, xv[i].x, ac[i].x);
+        ac[i].y = fma(d, xv[i].y, ac[i].y);
+      }
+    }
+    if (has_e) {
+      mbar_wait(&bars[2], ephase);
+      ephase ^= 1u;
+    }
+    cplx* po = A.out + g0;
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      double cr = ac[i].x, ci = ac[i].y;
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
+      if (has_e) {
+        const cplx u = ebuf[tid + i * NT];
+        cr = fma(ecoef, u.x, cr);
+        ci = fma(ecoef, u.y, ci);
+      }
+      if (LANCZOS) {
+        cr = fma(-axs, xv[i].x, cr);
+        ci = fma(-axs, xv[i].y, ci);
+        acc_n = fma(cr, cr, fma(ci, ci, acc_n));
+      }
+      ac[i] = make_double2(cr, ci);
+      st_stream(po + i * S, ac[i]);
+    }
+
+    if (LANCZOS && A.qsweep) {
+      __syncthreads();
+      cplx* sw = xbuf + stage * TILE;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
+      __syncthreads();
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        double hr = 0.0, hi = 0.0;
+        #pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          if ((i >> b) & 1) continue;
+          hr = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].x, hr);
+          hi = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].y, hi);
+        }
+        if (DIAG) {
+          double d = dr.d[i];
+          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+          hr = fma(d, ac[i].x, hr);
+          hi = fma(d, ac[i].y, hi);
+        }
+        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
+      }
+      for (int f = 0; f < A.fl.count; ++f) {
+        const int m = A.fl.mask[f];
+        if (tid & m) continue;
+        const cplx* ps = sw + (tid ^ m);
+        const double c2 = 2.0 * A.fl.coef[f];
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const cplx p = ps[i * NT];
+          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
+        }
+      }
+      fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
+    }
+  }
+  acc_a *= xs;
+
+  if (KIND == PASS_LAST_APPLY) return;
+  double mine[3];
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = block_sum<NT>(acc_n, red);
+  mine[2] = block_sum<NT>(acc_q, red);
+  double tot[3];
+  if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
+  if (threadIdx.x != 0) return;
+  double* scw = A.sc;
+  if (KIND == PASS_FIRST) {
+    scw[SC_AP + A.j] = tot[0];
+  } else if (KIND == PASS_MID) {
+    scw[SC_AP + A.j] += tot[0];
+  } else {
     const double nrm2 = tot[1];
     const double beta = sqrt(nrm2);
     scw[SC_AL + A.j] = alpha;
@@ -689,6 +970,14 @@ cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, in
 template <int TB, int KIND, bool DIAG>
 cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   constexpr int NT = pass_threads(TB);
+#if RSV_TMA
+  if constexpr (TB >= 3) {
+    static int occ_tma = 0;
+    constexpr size_t smem_tma = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+    return launch_persistent(pass_kernel_tma<TB, KIND, NT, DIAG>, args, args.sh.n_tiles, NT, smem_tma, &occ_tma,
+                             st);
+  }
+#endif
   constexpr int STAGES = TB >= 8 ? RSV_STAGES : 2;
   static int occ = 0;
   constexpr size_t smem = (STAGES + 1) * (1 << TB) * sizeof(cplx) + STAGES * 16 * sizeof(double);

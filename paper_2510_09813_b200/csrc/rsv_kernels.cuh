@@ -26,6 +26,7 @@
 // reduces ||w_j||^2 and q_{j+1}. Vectors are kept unnormalised with scales in a
 // device scalar array, so normalisation costs no pass.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -93,7 +94,17 @@ struct DiagArgs {
   double delta[kMaxQubits]; // detunings
 };
 
-struct PassArgs {
+// How a pass kernel moves a tile into shared memory (TMA path).
+enum TileLoad : int {
+  LOAD_RUNS = 0,       // per-warp cp.async.bulk of each contiguous run
+  LOAD_CONTIG = 1,     // the tile is one contiguous range: a single bulk copy
+  LOAD_TENSOR = 2,     // 5-D TMA tensor map (box = the whole strided tile)
+};
+
+struct alignas(64) PassArgs {
+  CUtensorMap tm_x;                     // TMA descriptors (LOAD_TENSOR) for x and ein
+  CUtensorMap tm_e;
+  int load;                             // TileLoad
   Shape sh;
   FlipSet fl;
   DiagArgs dg;

@@ -240,3 +240,44 @@ class TestObservables:
             phi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
             assert abs(rs.overlap(psi, phi) - np.vdot(psi, phi)) <= 1e-10 * abs(np.vdot(psi, phi))
             assert abs(rs.norm_difference(psi, phi) - np.linalg.norm(psi - phi)) <= 1e-12 * np.linalg.norm(psi)
+
+
+class TestFullSize:
+    """BASELINE configs[3] size (N=29) through size-independent properties."""
+
+    @pytest.fixture(scope="class")
+    def setup29(self, rs, torch):
+        from paper_2510_09813_b200 import workloads
+        from paper_2510_09813_b200.engine import SvEngine
+
+        reg, seq = workloads.config("random29")
+        u = rs.interaction_matrix(reg)
+        eng = SvEngine(29, u, diag="fly", max_krylov_dim=100, krylov_vectors_cap=10)
+        yield rs, torch, reg, seq, u, eng
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+
+    def test_norm_energy_and_reversibility(self, setup29):
+        rs, torch, reg, seq, u, eng = setup29
+        for k in range(12):   # into the pulse: a spread-out state
+            eng.step(*seq.step(k), 10.0, 1e-10, 100, next_params=seq.step(k + 1))
+        k = 12
+        om, de = seq.step(k)
+        s = rs.HamiltonianSlice.from_parameters(om, de, u)
+        psi0 = eng.state().clone()
+        h0 = rs.apply_hamiltonian(s, psi0)
+        e0 = rs.overlap(psi0, h0).real
+        del h0
+        rep = eng.step(om, de, 10.0, 1e-10, 100)
+        assert rep.converged
+        psi1 = eng.state()
+        assert abs(math.sqrt(rs.overlap(psi1, psi1).real) - 1.0) <= 1e-9
+        h1 = rs.apply_hamiltonian(s, psi1)
+        e1 = rs.overlap(psi1, h1).real
+        del h1
+        assert abs(e1 - e0) <= 1e-8 * max(1.0, abs(e0))
+        assert abs(rep.alpha0 - e0) <= 1e-9 * max(1.0, abs(e0))   # Energy observable = alpha_0
+        back = eng.step(om, de, -10.0, 1e-10, 100)
+        assert back.converged
+        assert rs.norm_difference(eng.state(), psi0) <= 1e-8
