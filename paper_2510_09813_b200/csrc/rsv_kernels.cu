@@ -590,8 +590,10 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const _
     }
 
     if (LANCZOS && A.qsweep) {
-      __syncthreads();
-      cplx* sw = xbuf + stage * TILE;
+      // w goes to the e buffer: each thread overwrites only the entries it alone has read,
+      // so a single barrier (w complete) suffices; the next refill of the buffer is issued
+      // after the next tile barrier
+      cplx* sw = ebuf;
       #pragma unroll
       for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
       __syncthreads();
