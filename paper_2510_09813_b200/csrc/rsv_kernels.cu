@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const _
 // q_0 (q-sweep with the next step's coefficients) and the observable masks. Observables
 // are reduced per warp into shared rows (no block barriers inside the tile loop).
 template <int TB, int NT>
-__global__ void __launch_bounds__(NT, 2) combine_kernel(const __grid_constant__ CombineArgs A) {
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __grid_constant__ CombineArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -677,17 +677,25 @@ __global__ void __launch_bounds__(NT, 2) combine_kernel(const __grid_constant__ 
 
   for (uint64_t t = blockIdx.x; t < A.sh.n_tiles; t += gridDim.x) {
     const uint64_t g0 = tile_index(A.sh, t, tid);
-    cplx wv[EPT];
+    cplx wv[EPT], cur[EPT], nxt[EPT];
     #pragma unroll
-    for (int i = 0; i < EPT; ++i) wv[i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < EPT; ++i) {
+      wv[i] = make_double2(0.0, 0.0);
+      cur[i] = ld_stream(A.v[0] + g0 + off[i]);
+    }
+    // register double buffer: vector k+1 is in flight while vector k is accumulated
     for (int k = 0; k < A.k; ++k) {
-      const cplx* vk = A.v[k] + g0;
+      if (k + 1 < A.k) {
+        const cplx* vn = A.v[k + 1] + g0;
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) nxt[i] = ld_stream(vn + off[i]);
+      }
       const double2 c = A.coef[k];
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        const cplx x = ld_stream(vk + off[i]);
-        wv[i].x = fma(c.x, x.x, fma(-c.y, x.y, wv[i].x));
-        wv[i].y = fma(c.x, x.y, fma(c.y, x.x, wv[i].y));
+        wv[i].x = fma(c.x, cur[i].x, fma(-c.y, cur[i].y, wv[i].x));
+        wv[i].y = fma(c.x, cur[i].y, fma(c.y, cur[i].x, wv[i].y));
+        cur[i] = nxt[i];
       }
     }
     #pragma unroll

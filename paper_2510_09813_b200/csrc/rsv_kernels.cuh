@@ -47,7 +47,7 @@ constexpr int kGcStride = 14;     // lo-pass tile table row: gc[0..11], hh, tb (
 #define RSV_PASS_THREADS 512
 #endif
 constexpr int pass_threads(int tb) { return (1 << tb) < RSV_PASS_THREADS ? (1 << tb) : RSV_PASS_THREADS; }
-constexpr int combine_threads(int tb) { return (1 << tb) < 256 ? (1 << tb) : 256; }
+constexpr int combine_threads(int tb) { return (1 << tb) < 512 ? (1 << tb) : 512; }
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
 // scalar slots (device double array, reset per step)
