@@ -226,12 +226,13 @@ def alg_bytes_per_launch(family, n, k_avg, diag):
 
     lo   : read s_j (16 B) + s_{j-1} (16 B, all but the first iteration of a step) + write u (16 B)
            (+ 8 B of precomputed diagonal for diag='vec')
+    chunk: the same bytes for two bit groups (its second tile pass re-reads s_j and u' from L2)
     mid  : read s_j + u, write u            (48 B)
     last : read s_j + u, write s_{j+1}      (48 B)
     combine : read the k basis vectors, write psi ((k + 1) x 16 B)
     """
     amp = 2 ** n
-    if family == "lo":
+    if family in ("lo", "chunk"):
         prev_frac = (k_avg - 1.0) / k_avg if k_avg > 0 else 0.0
         return (32 + 16 * prev_frac + (8 if diag == "vec" else 0)) * amp
     if family in ("mid", "last"):
@@ -256,6 +257,8 @@ def run_ours(args):
     u = interaction_matrix(reg)
     t_setup = time.time()
     eng = SvEngine(n, u, diag=args.diag, max_krylov_dim=cfg.max_krylov_dim)
+    if args.plan_gm != -1:
+        eng.set_plan(args.plan_gm)
     eng.set_observables([1 << q for q in range(n)])
     plan = eng.pass_plan()
     stream = torch.cuda.current_stream()
@@ -411,6 +414,8 @@ def main(argv=None):
     ap.add_argument("--dt", type=int, default=10)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--diag", default="fly", choices=["fly", "vec"])
+    ap.add_argument("--plan-gm", type=int, default=-1,
+                    help="pass plan: -1 auto, 0 plain bit-group passes, 3..9 L2 chunk pass (A/B runs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

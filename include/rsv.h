@@ -110,7 +110,12 @@ int rsv_axpy(rsv_context* ctx, void* y, const void* x, double a_re, double a_im,
 int rsv_scale(rsv_context* ctx, void* y, const void* x, double a_re, double a_im, uint64_t n);
 
 /* Introspection / measurement support. */
-int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* per pass: a, p, g, kind */
+int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass: a, p, g, lo, family, chunk_gm] */
+/* Pass-plan override (tests / tuning): chunk_group_bits -1 = auto (chunk pass at N >= 22), 0 = plain
+ * bit-group passes, 3..9 = force the L2-resident chunk pass over bits [0, 12 + g); chunk_lag = M tiles
+ * handed out ahead of the first L tile (-1 = auto, 1.5 chunks). No reference counterpart: the reference
+ * has one matvec loop (rydsim/_kernels.py:14). */
+int rsv_set_plan(rsv_context* ctx, int chunk_group_bits, long long chunk_lag);
 int rsv_set_profiling(rsv_context* ctx, int on);
 /* per kernel family: [0]=lo pass, [1]=mid passes, [2]=last pass, [3]=combine; ms and launches */
 int rsv_get_profile(rsv_context* ctx, double* ms4, long long* launches4);

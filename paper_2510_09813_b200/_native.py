@@ -77,6 +77,7 @@ SIGNATURES = {
     "rsv_scale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_uint64]),
     "rsv_pass_plan": (ctypes.c_int, [ctypes.c_void_p, c_int_p, ctypes.c_int]),
+    "rsv_set_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]),
     "rsv_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_get_profile": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_ll_p]),
     "rsv_reset_profile": (ctypes.c_int, [ctypes.c_void_p]),

@@ -191,6 +191,11 @@ struct PassPlan {
   rsv::Shape sh;
   std::vector<int> qubits;   // qubits whose flips this pass applies (all inside its tile)
   bool lo;    // lo tile (bits [0, a)) carries the diagonal
+  // chunk pass (rsv::ChunkArgs): sh/qubits are its L tiles, shm/qubits_m its M tiles
+  bool chunk = false;
+  int gm = 0;
+  rsv::Shape shm{};
+  std::vector<int> qubits_m;
 };
 
 }  // namespace
@@ -211,6 +216,10 @@ struct rsv_context {
   std::vector<void*> phys;        // bound slots
   std::vector<int> logical;       // logical slot -> physical; logical 0..K = Krylov s_j, K+1 = work
   std::vector<PassPlan> plan;
+  int plan_gm = -1;               // chunk group bits: -1 auto, 0 off, 3..9 forced (rsv_set_plan)
+  long long plan_lag = -1;        // chunk scheduler lag in M tiles (-1 auto)
+  unsigned long long* d_ticket = nullptr;
+  unsigned* d_done = nullptr;     // per-chunk M-tile counters (2^(n-15) entries: any gm >= 3)
   std::vector<double> h_u;
   // caches
   bool prep_valid = false;
@@ -252,17 +261,34 @@ cplx* work(const rsv_context* c) { return slot(c, (int)c->logical.size() - 1); }
 #endif
 constexpr int kDelegateLow = RSV_DELEGATE_LOW;
 
-void build_plan(rsv_context* c) {
-  const int n = c->n;
-  c->plan.clear();
-  const int alo = std::min(n, rsv::kLoBits);
-  PassPlan lo;
-  lo.sh = rsv::Shape{n, alo, alo, 0, 1ull << (n - alo)};
-  for (int q = 0; q < alo; ++q) lo.qubits.push_back(q);
-  lo.lo = true;
-  c->plan.push_back(lo);
-  const int rem = n - alo;
-  if (rem <= 0) return;
+#ifndef RSV_CHUNK_GM
+#define RSV_CHUNK_GM 8
+#endif
+#ifndef RSV_CHUNK_AUTO
+#define RSV_CHUNK_AUTO 0
+#endif
+
+// Chunk group bits for N qubits under the context's setting (0 = plain passes).
+int chunk_gm_for(int n, int setting) {
+  if (setting == 0) return 0;
+  // M tiles keep a = 12 - gm <= log2(pass threads) so a thread's amplitudes sit at one stride
+  const int gmin = std::max(3, rsv::kLoBits - rsv::ilog2(rsv::pass_threads(rsv::kLoBits)));
+  if (setting > 0) return (setting >= gmin && setting <= 9 && n - rsv::kLoBits - setting >= 1) ? setting : 0;
+  // auto: off. Measured at N=29 ("L2-resident chunk pass"): the chunk pass cuts a
+  // Lanczos iteration's HBM bytes from 144 to 96 per amplitude, but its two tile passes stay
+  // shared-memory-pipe bound, so the plain passes (HBM-bound at ~0.95 of the copy peak) are faster.
+#if RSV_CHUNK_AUTO
+  if (n - rsv::kLoBits > rsv::kLoBits - 3) return std::min(RSV_CHUNK_GM, n - rsv::kLoBits - 1);
+#endif
+  return 0;
+}
+
+// Groups of <= 9 bits covering [from, n), smallest at the top of the index, in execution order
+// (lowest group last unless RSV_LAST_TOP).
+std::vector<PassPlan> hi_groups(int n, int from) {
+  std::vector<PassPlan> out;
+  const int rem = n - from;
+  if (rem <= 0) return out;
   const int gmax = rsv::kLoBits - 3;
   const int ng = (rem + gmax - 1) / gmax;
   std::vector<int> sizes;   // ascending: the top (most strided) groups are the smallest
@@ -281,15 +307,50 @@ void build_plan(rsv_context* c) {
     hi.push_back(p);
     top -= s;
   }
-  // execution order: lo, the top groups, last = the lowest group (least strided: its q-sweep and
-  // its write of the next Krylov vector stream best there)
 #if RSV_LAST_TOP
-  for (size_t i = hi.size() - 1; i >= 1; --i) c->plan.push_back(hi[i]);
-  c->plan.push_back(hi[0]);
+  for (size_t i = hi.size() - 1; i >= 1; --i) out.push_back(hi[i]);
+  out.push_back(hi[0]);
 #else
-  for (size_t i = 0; i + 1 < hi.size(); ++i) c->plan.push_back(hi[i]);
-  c->plan.push_back(hi.back());
+  for (size_t i = 0; i + 1 < hi.size(); ++i) out.push_back(hi[i]);
+  out.push_back(hi.back());
 #endif
+  return out;
+}
+
+#ifndef RSV_CHUNK_DELEGATE
+#define RSV_CHUNK_DELEGATE 3
+#endif
+
+void build_plan(rsv_context* c) {
+  const int n = c->n;
+  c->plan.clear();
+  const int alo = std::min(n, rsv::kLoBits);
+  PassPlan lo;
+  lo.sh = rsv::Shape{n, alo, alo, 0, 1ull << (n - alo)};
+  for (int q = 0; q < alo; ++q) lo.qubits.push_back(q);
+  lo.lo = true;
+  const int gm = chunk_gm_for(n, c->plan_gm);
+  if (gm > 0) {
+    // chunk pass: L tiles = the lo tile, M tiles = 2^(12-gm) contiguous x bits [12, 12+gm)
+    lo.chunk = true;
+    lo.gm = gm;
+    lo.shm = rsv::Shape{n, rsv::kLoBits - gm, rsv::kLoBits, gm, 1ull << (n - rsv::kLoBits)};
+    for (int q = rsv::kLoBits; q < rsv::kLoBits + gm; ++q) lo.qubits_m.push_back(q);
+    c->plan.push_back(lo);
+    for (auto& p : hi_groups(n, rsv::kLoBits + gm)) c->plan.push_back(p);
+    // the lowest bits' flips move to the first hi pass (its tile holds them too): the chunk
+    // pass carries two tiles' worth of shared-memory work per amplitude
+    const int d = RSV_CHUNK_DELEGATE;
+    if (d > 0 && c->plan[1].sh.a >= d) {
+      PassPlan& l = c->plan[0];
+      PassPlan& m = c->plan[1];
+      l.qubits.erase(l.qubits.begin(), l.qubits.begin() + d);
+      for (int q = 0; q < d; ++q) m.qubits.push_back(q);
+    }
+    return;
+  }
+  c->plan.push_back(lo);
+  for (auto& p : hi_groups(n, alo)) c->plan.push_back(p);
   if (kDelegateLow > 0 && c->plan.size() >= 3 && c->plan[1].sh.a >= kDelegateLow && alo > kDelegateLow) {
     PassPlan& l = c->plan[0];
     PassPlan& m = c->plan[1];
@@ -441,10 +502,55 @@ int prepare(rsv_context* c, const double* omegas, const double* deltas) {
   return RSV_OK;
 }
 
+// The chunk pass (first kernel of an iteration): out = (A_M + A_L + D) v - beta' prev.
+int launch_chunk_pass(rsv_context* c, const PassPlan& p, const double* omegas, const double* deltas,
+                      const cplx* x, int x_scale_slot, const cplx* prev, cplx* out, int j) {
+  rsv::ChunkArgs A{};
+  A.shm = p.shm;
+  A.shl = p.sh;
+  PassPlan pm;
+  pm.sh = p.shm;
+  pm.qubits = p.qubits_m;
+  pm.lo = false;
+  const int nt = rsv::pass_threads(rsv::kLoBits);
+  A.flm = flips_for(pm, omegas, nt);
+  A.fll = flips_for(p, omegas, nt);
+  A.dg = diag_for(c, p, deltas);
+  A.x = x;
+  A.x_scale_slot = x_scale_slot;
+  A.prev = prev;
+  A.out = out;
+  A.j = j;
+  A.gm = p.gm;
+  const unsigned long long tiles = 1ull << p.gm;
+  unsigned long long lag = c->plan_lag > 0 ? (unsigned long long)c->plan_lag : tiles + tiles / 2;
+  if (lag < tiles) lag = tiles;   // an L tile may never precede the M tiles of its chunk
+  A.lag = std::min<unsigned long long>(lag, p.sh.n_tiles);
+  A.sc = c->d_sc;
+  A.part = c->d_part;
+  A.counter = c->d_counter;
+  A.ticket = c->d_ticket;
+  A.done = c->d_done;
+  A.load_m = rsv::LOAD_RUNS;
+  if (RSV_TENSOR_MAPS && p.shm.a <= 7 && encode_tile_map(&A.tm_x, x, p.shm) &&
+      (prev == nullptr || encode_tile_map(&A.tm_e, prev, p.shm)))
+    A.load_m = rsv::LOAD_TENSOR;
+  prof_begin(c, 0);
+  CUDA_TRY(rsv::launch_chunk(A, c->st));
+  prof_end(c);
+  return RSV_OK;
+}
+
 int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const double* deltas) {
   const size_t np = c->plan.size();
   for (size_t pi = 0; pi < np; ++pi) {
     const PassPlan& p = c->plan[pi];
+    if (p.chunk) {
+      int rc = launch_chunk_pass(c, p, omegas, deltas, slot(c, j), rsv::SC_SG + j, j > 0 ? slot(c, j - 1) : nullptr,
+                                 work(c), j);
+      if (rc) return rc;
+      continue;
+    }
     rsv::PassArgs A{};
     const bool last = pi + 1 == np;
     A.kind = last ? rsv::PASS_LAST_LANCZOS : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
@@ -657,6 +763,11 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_dl, sizeof(double) << rsv::kLoBits);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_gc, sizeof(double) * rsv::kGcStride * gc_rows);
+  const size_t done_rows = n_qubits > 15 ? size_t(1) << (n_qubits - 15) : 1;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_ticket, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_done, sizeof(unsigned) * done_rows);
+  if (e == cudaSuccess) e = cudaMemset(c->d_ticket, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, sizeof(unsigned) * done_rows);
 
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_pin, sizeof(double) * rsv::SC_SIZE);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->obs_event, cudaEventDisableTiming);
@@ -684,6 +795,8 @@ void rsv_destroy(rsv_context* c) {
   cudaFree(c->d_counter);
   cudaFree(c->d_dl);
   cudaFree(c->d_gc);
+  cudaFree(c->d_ticket);
+  cudaFree(c->d_done);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->obs_event) cudaEventDestroy(c->obs_event);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -751,6 +864,12 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
   if (rc) return rc;
   for (size_t pi = 0; pi < np; ++pi) {
     const PassPlan& p = c->plan[pi];
+    if (p.chunk) {
+      rc = launch_chunk_pass(c, p, omegas, deltas, reinterpret_cast<const cplx*>(psi), rsv::SC_ONE, nullptr,
+                             reinterpret_cast<cplx*>(out), kScratchJ);
+      if (rc) return rc;
+      continue;
+    }
     rsv::PassArgs A{};
     A.kind = pi + 1 == np ? rsv::PASS_LAST_APPLY : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
@@ -912,15 +1031,32 @@ int rsv_scale(rsv_context* c, void* y, const void* x, double are, double aim, ui
 int rsv_pass_plan(rsv_context* c, int* out, int max_ints) {
   if (!c) return fail(RSV_ERR_ARG, "NULL context");
   const int np = (int)c->plan.size();
-  if (max_ints < 1 + 5 * np) return fail(RSV_ERR_ARG, "buffer too small");
+  if (max_ints < 1 + 6 * np) return fail(RSV_ERR_ARG, "buffer too small");
   out[0] = np;
   for (int i = 0; i < np; ++i) {
-    out[1 + 5 * i] = c->plan[i].sh.a;
-    out[2 + 5 * i] = c->plan[i].sh.p;
-    out[3 + 5 * i] = c->plan[i].sh.g;
-    out[4 + 5 * i] = c->plan[i].lo ? 1 : 0;
-    out[5 + 5 * i] = family_of(i, np);
+    out[1 + 6 * i] = c->plan[i].sh.a;
+    out[2 + 6 * i] = c->plan[i].sh.p;
+    out[3 + 6 * i] = c->plan[i].sh.g;
+    out[4 + 6 * i] = c->plan[i].lo ? 1 : 0;
+    out[5 + 6 * i] = family_of(i, np);
+    out[6 + 6 * i] = c->plan[i].chunk ? c->plan[i].gm : 0;
   }
+  return RSV_OK;
+}
+
+int rsv_set_plan(rsv_context* c, int chunk_group_bits, long long chunk_lag) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (chunk_group_bits != -1 && chunk_group_bits != 0 && (chunk_group_bits < 3 || chunk_group_bits > 9))
+    return fail(RSV_ERR_ARG, "chunk_group_bits must be -1 (auto), 0 (off) or 3..9, got %d", chunk_group_bits);
+  if (chunk_group_bits > 0 && chunk_gm_for(c->n, chunk_group_bits) == 0)
+    return fail(RSV_ERR_ARG, "chunk group of %d bits is invalid at N=%d (needs M tiles of <= 2^%d contiguous and a hi pass)",
+                chunk_group_bits, c->n, rsv::ilog2(rsv::pass_threads(rsv::kLoBits)));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->plan_gm = chunk_group_bits;
+  c->plan_lag = chunk_lag;
+  build_plan(c);
+  c->prep_valid = false;
+  c->dl_valid = false;
   return RSV_OK;
 }
 

@@ -207,7 +207,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 template <int TB, int KIND, int NT, bool DIAG>
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __grid_constant__ PassArgs A) {
+__global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kernel(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel(const __gri
 //   e buf  : this tile's elementwise operand, requested after the same barrier, awaited
 //            just before the epilogue
 template <int TB, int KIND, int NT, bool DIAG>
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const __grid_constant__ PassArgs A) {
+__global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kernel_tma(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const _
     mbar_init_fence();
   }
   __syncthreads();
-  unsigned xphase[2] = {0u, 0u}, ephase = 0u;
+  unsigned xphase = 0u, ephase = 0u;   // bit s = parity of x stage s (a register, not a local array)
   // prologue: tile blockIdx.x into stage 0
   if (blockIdx.x < ntiles) {
     if (tid == 0) mbar_arrive_expect_tx(&bars[0], tile_bytes);
@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const _
       if (tn < ntiles) mbar_arrive_expect_tx(&bars[stage ^ 1], tile_bytes);
       if (has_e) mbar_arrive_expect_tx(&bars[2], TILE * sizeof(cplx));
     }
-    mbar_wait(&bars[stage], xphase[stage]);
-    xphase[stage] ^= 1u;
+    mbar_wait(&bars[stage], (xphase >> stage) & 1u);
+    xphase ^= 1u << stage;
     __syncthreads();   // everyone is done with tile t-G: its x buffer and the e buffer are free
     if (tn < ntiles) {
       issue(A.x, &A.tm_x, tn, xbuf + (stage ^ 1) * TILE, &bars[stage ^ 1]);
@@ -650,6 +650,302 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) pass_kernel_tma(const _
     scw[SC_BE + A.j] = beta;
     scw[SC_SG + A.j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
     scw[SC_Q + A.j + 1] = nrm2 > 0.0 ? tot[2] / nrm2 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- L2-resident chunk pass
+// See ChunkArgs (rsv_kernels.cuh). Work item k in [0, 2 Nt) -> (kind, tile):
+//   k < lag                 : M tile k
+//   lag <= k < 2 Nt - lag   : alternating M tile lag + (k-lag)/2 and L tile (k-lag)/2
+//   k >= 2 Nt - lag         : the remaining L tiles
+// so an L tile of chunk c is handed out ~(lag - 2^gm) x 2 items after the last M tile of c.
+// Items come from one atomic ticket (fetched one item ahead, so its latency is hidden); an L
+// tile's operand u' is requested only after thread 0 has acquired the chunk's M counter.
+#ifndef RSV_CHUNK_HINTS
+#define RSV_CHUNK_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_hint(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 int c3, int c4, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;"
+      ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+        "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(cplx* p, cplx v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct ChunkItem {
+  bool is_l;
+  uint64_t t;
+};
+__device__ __forceinline__ ChunkItem chunk_item(uint64_t k, uint64_t nt, uint64_t lag) {
+  if (k < lag) return {false, k};
+  if (k < 2 * nt - lag) {
+    const uint64_t rel = k - lag;
+    return (rel & 1) ? ChunkItem{true, rel >> 1} : ChunkItem{false, lag + (rel >> 1)};
+  }
+  return {true, nt - lag + (k - (2 * nt - lag))};
+}
+
+template <int NT, bool DIAG>
+__global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ ChunkArgs A) {
+  constexpr int TILE = 1 << kLoBits;
+  constexpr int EPT = TILE / NT;
+  constexpr int RB = RegBits<EPT>::value;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  cplx* xbuf = reinterpret_cast<cplx*>(smem_al);             // [2][TILE]
+  cplx* ebuf = xbuf + 2 * TILE;                               // [TILE]
+  double* rows = reinterpret_cast<double*>(ebuf + TILE);     // [2][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 32);   // xbar[0], xbar[1], ebar
+  __shared__ double red[32];
+  __shared__ unsigned long long s_item[2];   // next item (decoded), double-buffered by stage parity
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* sc = A.sc;
+  const double xs = sc[A.x_scale_slot];
+  const bool has_prev = A.prev != nullptr;
+  const double ecoef_m = has_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 0.0;
+  double acc_a = 0.0;
+  const uint64_t Sm = elem_offset(A.shm, NT), Sl = elem_offset(A.shl, NT);
+  const uint64_t nt = A.shl.n_tiles;
+  const uint64_t total = 2 * nt;
+  const uint64_t lag = A.lag;
+  const unsigned tiles_per_chunk = 1u << A.gm;
+#if RSV_CHUNK_HINTS
+  const uint64_t pol_keep = policy_evict_last();
+  const uint64_t pol_drop = policy_evict_first();
+#endif
+
+  // M-tile copy geometry (LOAD_RUNS: per-warp runs of R amplitudes)
+  const int R = (1 << A.shm.a) < 32 ? (1 << A.shm.a) : 32;
+  const int RUNS = 32 / R;
+  auto issue_m = [&](const cplx* base, const CUtensorMap* map, uint64_t tt, cplx* dst, uint64_t* bar, bool keep) {
+#if RSV_CHUNK_HINTS
+    const uint64_t pol = keep ? pol_keep : pol_drop;
+#endif
+    if (A.load_m == LOAD_TENSOR) {
+      if (tid == 0) {
+        const int m = A.shm.p - A.shm.a;
+#if RSV_CHUNK_HINTS
+        tma_load_5d_hint(dst, map, 0, (int)(tt & ((1ull << m) - 1ull)), 0, 0, (int)(tt >> m), bar, pol);
+#else
+        tma_load_5d(dst, map, 0, (int)(tt & ((1ull << m) - 1ull)), 0, 0, (int)(tt >> m), bar);
+#endif
+      }
+      return;
+    }
+    if (lane < RUNS) {
+      const uint32_t e0 = (uint32_t)(warp * 32 + lane * R);
+      const cplx* src = base + tile_index(A.shm, tt, e0);
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+#if RSV_CHUNK_HINTS
+        bulk_g2s_hint(dst + e0 + i * NT, src + i * Sm, R * sizeof(cplx), bar, pol);
+#else
+        bulk_g2s(dst + e0 + i * NT, src + i * Sm, R * sizeof(cplx), bar);
+#endif
+      }
+    }
+  };
+  // items travel decoded: code = tile << 1 | is_l, kEnd past the last item (thread 0 decodes)
+  constexpr unsigned long long kEnd = ~0ull;
+  auto encode = [&](unsigned long long raw) -> unsigned long long {
+    if (raw >= total) return kEnd;
+    const ChunkItem it = chunk_item(raw, nt, lag);
+    return (it.t << 1) | (it.is_l ? 1ull : 0ull);
+  };
+  auto issue_x = [&](unsigned long long code, int st) {
+    const ChunkItem it{(code & 1ull) != 0, code >> 1};
+    if (it.is_l) {
+      if (tid == 0) {
+#if RSV_CHUNK_HINTS
+        bulk_g2s_hint(xbuf + st * TILE, A.x + (it.t << kLoBits), TILE * sizeof(cplx), &bars[st], pol_drop);
+#else
+        bulk_g2s(xbuf + st * TILE, A.x + (it.t << kLoBits), TILE * sizeof(cplx), &bars[st]);
+#endif
+        if (DIAG) bulk_g2s(rows + st * 16, A.dg.gc + it.t * kGcStride, 112, &bars[st]);
+      }
+    } else {
+      issue_m(A.x, &A.tm_x, it.t, xbuf + st * TILE, &bars[st], true);
+    }
+  };
+  auto x_bytes = [&](unsigned long long code) -> unsigned {
+    return TILE * sizeof(cplx) + ((DIAG && (code & 1ull)) ? 112u : 0u);
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    mbar_init_fence();
+    s_item[1] = encode(atomicAdd(A.ticket, 1ull));
+  }
+  __syncthreads();
+  unsigned long long cur = s_item[1];
+  unsigned long long pend = 0;
+  if (tid == 0) pend = atomicAdd(A.ticket, 1ull);   // the item after cur (consumed next iteration)
+  unsigned xphase = 0u, ephase = 0u;   // bit s = parity of x stage s (a register, not a local array)
+  if (cur != kEnd) {
+    if (tid == 0) mbar_arrive_expect_tx(&bars[0], x_bytes(cur));
+    __syncthreads();
+    issue_x(cur, 0);
+  }
+  int stage = 0;
+  bool signal_pending = false;   // the previous item was an M tile whose writes are not yet published
+  uint64_t signal_chunk = 0;
+  while (cur != kEnd) {
+    const ChunkItem it{(cur & 1ull) != 0, cur >> 1};
+    const bool has_e = it.is_l || has_prev;
+    if (tid == 0) {
+      const unsigned long long nx = encode(pend);
+      s_item[stage] = nx;
+      pend = atomicAdd(A.ticket, 1ull);
+      if (nx != kEnd) mbar_arrive_expect_tx(&bars[stage ^ 1], x_bytes(nx));
+      if (has_e) mbar_arrive_expect_tx(&bars[2], TILE * sizeof(cplx));
+    }
+    mbar_wait(&bars[stage], (xphase >> stage) & 1u);
+    xphase ^= 1u << stage;
+    __syncthreads();   // tile cur-1 fully consumed and stored; s_item[stage] visible
+    const unsigned long long next = s_item[stage];
+    if (tid == 0 && signal_pending) red_release_gpu(A.done + signal_chunk, 1u);
+    signal_pending = false;
+    if (next != kEnd) issue_x(next, stage ^ 1);
+    const uint64_t chunk = it.t >> A.gm;
+    if (has_e) {
+      if (it.is_l) {
+        if (tid == 0) {
+          while (ld_acquire_gpu(A.done + chunk) < tiles_per_chunk) __nanosleep(64);
+          fence_proxy_async_global();   // generic-proxy writes of other CTAs -> async-proxy (TMA) reads
+#if RSV_CHUNK_HINTS
+          bulk_g2s_hint(ebuf, A.out + (it.t << kLoBits), TILE * sizeof(cplx), &bars[2], pol_drop);
+#else
+          bulk_g2s(ebuf, A.out + (it.t << kLoBits), TILE * sizeof(cplx), &bars[2]);
+#endif
+        }
+      } else {
+        issue_m(A.prev, &A.tm_e, it.t, ebuf, &bars[2], false);
+      }
+    }
+    const cplx* s = xbuf + stage * TILE;
+    const uint64_t g0 = it.is_l ? (it.t << kLoBits) + tid : tile_index(A.shm, it.t, tid);
+    const uint64_t S = it.is_l ? Sl : Sm;
+    const FlipSet& fl = it.is_l ? A.fll : A.flm;
+
+    cplx xv[EPT], ac[EPT];
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      xv[i] = s[tid + i * NT];
+      ac[i] = make_double2(0.0, 0.0);
+    }
+    #pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const double c = (it.is_l ? A.fll.rcoef[b] : A.flm.rcoef[b]) * xs;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        ac[i].x = fma(c, xv[i ^ (1 << b)].x, ac[i].x);
+        ac[i].y = fma(c, xv[i ^ (1 << b)].y, ac[i].y);
+      }
+    }
+    const int nfl = fl.count;
+    for (int f = 0; f < nfl; ++f) {
+      const cplx* ps = s + (tid ^ fl.mask[f]);
+      const double c = fl.coef[f] * xs;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const cplx p = ps[i * NT];
+        ac[i].x = fma(c, p.x, ac[i].x);
+        ac[i].y = fma(c, p.y, ac[i].y);
+      }
+    }
+    if (DIAG && it.is_l) {
+      DiagRow<NT, EPT> dr;
+      dr.setup(A.dg, A.shl, it.t, tid, rows + stage * 16);
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        double d = dr.d[i];
+        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+        d *= xs;
+        ac[i].x = fma(d, xv[i].x, ac[i].x);
+        ac[i].y = fma(d, xv[i].y, ac[i].y);
+      }
+    }
+    if (has_e) {
+      mbar_wait(&bars[2], ephase);
+      ephase ^= 1u;
+    }
+    const double ecoef = it.is_l ? 1.0 : ecoef_m;
+    cplx* po = A.out + g0;
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      double cr = ac[i].x, ci = ac[i].y;
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
+      if (has_e) {
+        const cplx u = ebuf[tid + i * NT];
+        cr = fma(ecoef, u.x, cr);
+        ci = fma(ecoef, u.y, ci);
+      }
+#if RSV_CHUNK_HINTS
+      st_hint(po + i * S, make_double2(cr, ci), it.is_l ? pol_drop : pol_keep);
+#else
+      st_stream(po + i * S, make_double2(cr, ci));
+#endif
+    }
+    if (!it.is_l) {
+      signal_pending = true;
+      signal_chunk = chunk;
+    }
+    cur = next;
+    stage ^= 1;
+  }
+  if (signal_pending) {
+    __syncthreads();
+    if (tid == 0) red_release_gpu(A.done + signal_chunk, 1u);
+  }
+  acc_a *= xs;
+
+  double mine[3];
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = 0.0;
+  mine[2] = 0.0;
+  double tot[3];
+  if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
+  // every CTA has left the item loop: reset the scheduler for the next launch
+  const uint64_t nchunks = nt >> A.gm;
+  for (uint64_t c = tid; c < nchunks; c += NT) A.done[c] = 0u;
+  if (tid == 0) {
+    *A.ticket = 0ull;
+    A.sc[SC_AP + A.j] = tot[0];
   }
 }
 
@@ -1018,6 +1314,15 @@ cudaError_t launch_pass_tb(const PassArgs& args, cudaStream_t st) {
   }
 }
 
+template <bool DIAG>
+cudaError_t launch_chunk_d(const ChunkArgs& args, cudaStream_t st) {
+  constexpr int NT = pass_threads(kLoBits);
+  static int occ = 0;
+  constexpr size_t smem = 3 * (1 << kLoBits) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+  // tiles are handed out dynamically: the grid only needs to be resident (persistent)
+  return launch_persistent(chunk_kernel<NT, DIAG>, args, 2 * args.shl.n_tiles, NT, smem, &occ, st);
+}
+
 template <int TB>
 cudaError_t launch_combine_tb(const CombineArgs& args, cudaStream_t st) {
   constexpr int NT = combine_threads(TB);
@@ -1061,6 +1366,11 @@ cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st) {
     case 12: return launch_combine_tb<12>(args, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_chunk(const ChunkArgs& args, cudaStream_t st) {
+  if (args.dg.mode != DIAG_NONE) return launch_chunk_d<true>(args, st);
+  return launch_chunk_d<false>(args, st);
 }
 
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,

@@ -134,9 +134,37 @@ struct CombineArgs {
   double* sc; double* part; unsigned* counter;
 };
 
+// L2-resident chunk pass (the first kernel of a Lanczos iteration at N >= 22).
+// A chunk = the 2^(12+gm) amplitudes sharing bits [12+gm, n). Two kinds of 4096-amplitude
+// tiles cover it: M tiles (2^(12-gm) contiguous x 2^gm rows strided along bits [12, 12+gm))
+// and L tiles (bits [0, 12) contiguous). One persistent kernel hands out M and L tiles from a
+// single ticket counter; the L tiles of a chunk start only once all of its M tiles are written
+// (per-chunk release/acquire counters), M running ~1.5 chunks ahead. The M tiles read x and
+// s_{j-1} from HBM and write the partial sum u' (kept in L2); the L tiles re-read x and u'
+// from L2 and write u = (A_M + A_L + D) v - beta' s_{j-1} -- one HBM round trip for two bit
+// groups. Everything else (reductions, scales, flips) is PASS_FIRST semantics.
+struct alignas(64) ChunkArgs {
+  CUtensorMap tm_x;                     // M-tile TMA descriptors over x and s_{j-1} (load_m == LOAD_TENSOR)
+  CUtensorMap tm_e;
+  int load_m;                           // TileLoad of the M tiles (LOAD_TENSOR or LOAD_RUNS)
+  Shape shm, shl;                       // M / L tile shapes (n_tiles equal)
+  FlipSet flm, fll;
+  DiagArgs dg;                          // diagonal (L tiles)
+  const cplx* x; int x_scale_slot;
+  const cplx* prev;                     // s_{j-1} (may be null: first iteration / plain H.psi)
+  cplx* out;                            // u' then u (in place)
+  int j;
+  int gm;                               // chunk group bits: 2^gm tiles of each kind per chunk
+  unsigned long long lag;               // M tiles handed out before the first L tile
+  double* sc; double* part; unsigned* counter;
+  unsigned long long* ticket;           // work counter (reset by the last CTA)
+  unsigned* done;                       // per-chunk finished M tiles (reset by the last CTA)
+};
+
 // host-side launchers (rsv_kernels.cu); persistent grids sized from the occupancy query
 cudaError_t launch_pass(const PassArgs& args, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st);
+cudaError_t launch_chunk(const ChunkArgs& args, cudaStream_t st);
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
                             double* dl, cudaStream_t st);
 cudaError_t launch_tile_table(int a, int n, const double* umat, double* gc, cudaStream_t st);

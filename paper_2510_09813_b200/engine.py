@@ -68,8 +68,18 @@ class Context:
         buf = (ctypes.c_int * 64)()
         nat.check(self.lib.rsv_pass_plan(self.ctx, buf, 64))
         n = buf[0]
-        return [dict(a=buf[1 + 5 * i], p=buf[2 + 5 * i], g=buf[3 + 5 * i], lo=bool(buf[4 + 5 * i]),
-                     family=("lo", "mid", "last")[buf[5 + 5 * i]]) for i in range(n)]
+        out = []
+        for i in range(n):
+            a, p, g, lo, fam, gm = (buf[1 + 6 * i + k] for k in range(6))
+            d = dict(a=a, p=p, g=g, lo=bool(lo), family=("lo", "mid", "last")[fam])
+            if gm:
+                d.update(family="chunk", chunk_bits=12 + gm, m_tile=dict(a=12 - gm, p=12, g=gm))
+            out.append(d)
+        return out
+
+    def set_plan(self, chunk_group_bits: int = -1, chunk_lag: int = -1):
+        """Pass-plan override (tests/tuning): -1 auto, 0 plain passes, 3..9 force the chunk pass."""
+        nat.check(self.lib.rsv_set_plan(self.ctx, int(chunk_group_bits), int(chunk_lag)), "rsv_set_plan")
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -200,5 +210,6 @@ class SvEngine(Context):
         ms = (ctypes.c_double * 4)()
         cnt = (ctypes.c_longlong * 4)()
         nat.check(self.lib.rsv_get_profile(self.ctx, ms, cnt))
-        names = ("lo", "mid", "last", "combine")
+        first = "chunk" if self.pass_plan()[0]["family"] == "chunk" else "lo"
+        names = (first, "mid", "last", "combine")
         return {names[i]: {"ms": ms[i], "launches": cnt[i]} for i in range(4)}

@@ -17,6 +17,7 @@ n = int(sys.argv[1])
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 reg, seq = workloads.config("random29", n_override=n)
 eng = SvEngine(n, interaction_matrix(reg), diag=os.environ.get("RSV_DIAG", "fly"), max_krylov_dim=100)
+eng.set_plan(int(os.environ.get("RSV_PLAN_GM", "-1")), int(os.environ.get("RSV_PLAN_LAG", "-1")))
 for k in range(3):
     eng.step(*seq.step(k), 10.0, 1e-10, 100, next_params=seq.step(k + 1))
 eng.set_profiling(True)
@@ -26,8 +27,8 @@ for k in range(3, 3 + steps):
     mv += r.matvecs
 prof = eng.profile()
 amp = 2 ** n
-alg = {"lo": 48 * amp, "mid": 48 * amp, "last": 48 * amp}   # x + elementwise operand + out
-out = {"lib": os.environ.get("RSV_LIB", "default"), "n": n, "matvecs": mv}
+alg = {"lo": 48 * amp, "chunk": 48 * amp, "mid": 48 * amp, "last": 48 * amp}   # x + elementwise operand + out
+out = {"lib": os.environ.get("RSV_LIB", "default"), "n": n, "matvecs": mv, "gm": os.environ.get("RSV_PLAN_GM", "-1"), "lag": os.environ.get("RSV_PLAN_LAG", "-1")}
 for f, v in prof.items():
     if v["launches"] and f in alg:
         ms = v["ms"] / v["launches"]
