@@ -55,9 +55,10 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
 void rsv_destroy(rsv_context* ctx);
 int rsv_set_stream(rsv_context* ctx, void* stream);
 
-/* Bind caller-allocated (e.g. torch) device vectors: nslots >= 3 vectors of 2^n complex128.
- * Slot layout: Krylov basis s_0..s_{nslots-2} (s_0 = state) and one work vector.
- * The Krylov cap is nslots - 2 vectors; steps needing more are split (exactly) in time. */
+/* Bind caller-allocated (e.g. torch) device vectors: nslots >= 2 vectors of 2^n complex128.
+ * Slot layout: Krylov basis s_0..s_{nslots-2} (s_0 = state); Lanczos iteration j keeps its partial
+ * sums in slot j+1 and turns them into s_{j+1} in place, so the last slot needs no basis vector.
+ * The Krylov cap is nslots - 1 vectors; steps needing more are split (exactly) in time. */
 int rsv_bind_slots(rsv_context* ctx, void* const* slots, int nslots);
 /* Index of the bound slot currently holding the state (changes after every step). */
 int rsv_state_slot(rsv_context* ctx, int* out);

@@ -241,11 +241,13 @@ struct rsv_context {
 
 namespace {
 
-int kcap(const rsv_context* c) { return (int)c->logical.size() - 2; }
+// Slots 0..K: s_0 (the state) .. s_{K-1} are the Krylov basis; the partial sums u of iteration j
+// live in slot j+1 (each pass reads and rewrites its own tiles in place, the last pass turns u
+// into s_{j+1} there), so no separate work vector is needed and K = nslots - 1.
+int kcap(const rsv_context* c) { return (int)c->logical.size() - 1; }
 cplx* slot(const rsv_context* c, int logical_index) {
   return reinterpret_cast<cplx*>(c->phys[c->logical[logical_index]]);
 }
-cplx* work(const rsv_context* c) { return slot(c, (int)c->logical.size() - 1); }
 
 // Pass plan: the lo pass (tile = bits [0, 12), carries the diagonal) and hi passes over groups
 // of <= 9 high bits (tile = 2^a contiguous x 2^g strided rows). Smaller groups sit at the top
@@ -547,7 +549,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     const PassPlan& p = c->plan[pi];
     if (p.chunk) {
       int rc = launch_chunk_pass(c, p, omegas, deltas, slot(c, j), rsv::SC_SG + j, j > 0 ? slot(c, j - 1) : nullptr,
-                                 work(c), j);
+                                 slot(c, j + 1), j);
       if (rc) return rc;
       continue;
     }
@@ -568,10 +570,10 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
       A.ein = j > 0 ? slot(c, j - 1) : nullptr;
       A.ein_is_prev = 1;
     } else {
-      A.ein = work(c);
+      A.ein = slot(c, j + 1);
       A.ein_is_prev = 0;
     }
-    A.out = last ? slot(c, j + 1) : work(c);
+    A.out = slot(c, j + 1);   // u in place, then s_{j+1}
     A.qsweep = last ? 1 : 0;
     set_tile_load(A);
     prof_begin(c, family_of(pi, np));
@@ -682,9 +684,9 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
   const bool more = frac < 1.0;
   const double* qo = more ? omegas : q_omegas;
   const double* qd = more ? deltas : q_deltas;
-  rc = run_combine(c, k, coef, work(c), qo, qd, (!more && last_run && observe) ? 1 : 0);
+  // elementwise, so in place: every amplitude of s_0 is read before it is overwritten
+  rc = run_combine(c, k, coef, slot(c, 0), qo, qd, (!more && last_run && observe) ? 1 : 0);
   if (rc) return rc;
-  std::swap(c->logical[0], c->logical[c->logical.size() - 1]);
   if (qo != nullptr) {
     c->prep_key = prep_key_for(c, qo, qd);
     c->prep_valid = true;
@@ -811,9 +813,9 @@ int rsv_set_stream(rsv_context* c, void* stream) {
 
 int rsv_bind_slots(rsv_context* c, void* const* slots, int nslots) {
   if (!c) return fail(RSV_ERR_ARG, "NULL context");
-  if (nslots < 3) return fail(RSV_ERR_ARG, "need at least 3 slots (2 Krylov vectors + work), got %d", nslots);
-  if (nslots - 2 > rsv::kMaxKrylov)
-    nslots = rsv::kMaxKrylov + 2;   // extra slots are never used
+  if (nslots < 2) return fail(RSV_ERR_ARG, "need at least 2 slots (state + one Lanczos vector), got %d", nslots);
+  if (nslots - 1 > rsv::kMaxKrylov)
+    nslots = rsv::kMaxKrylov + 1;   // extra slots are never used
   c->phys.assign(slots, slots + nslots);
   for (int i = 0; i < nslots; ++i) {
     if (c->phys[i] == nullptr || (reinterpret_cast<uintptr_t>(c->phys[i]) & 15u))

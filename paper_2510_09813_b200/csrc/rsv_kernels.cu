@@ -971,28 +971,50 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
   #pragma unroll
   for (int i = 0; i < EPT; ++i) off[i] = elem_offset(A.sh, i * NT);
 
+  // The k vectors of a tile stream through a 3-stage cp.async ring (two items in flight per
+  // thread). Each thread copies and reads only its own amplitudes, so the ring needs no block
+  // barriers; the q-sweep reuses the stage of a tile's last vector.
+  constexpr int RING = 3;
+  const uint64_t G = gridDim.x;
+  const int kv = A.k;
+  uint64_t is_t = blockIdx.x;   // next (tile, vector, stage) to request
+  int is_v = 0, is_s = 0;
+  auto issue_next = [&]() {
+    if (is_t < A.sh.n_tiles) {
+      const cplx* src = A.v[is_v] + tile_index(A.sh, is_t, tid);
+      cplx* dst = s + is_s * TILE + tid;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) cp_async16(dst + i * NT, src + off[i]);
+      if (++is_v == kv) {
+        is_v = 0;
+        is_t += G;
+      }
+    }
+    cp_async_commit();
+    is_s = is_s == RING - 1 ? 0 : is_s + 1;
+  };
+  issue_next();
+  issue_next();
+  int stage = 0;
   for (uint64_t t = blockIdx.x; t < A.sh.n_tiles; t += gridDim.x) {
     const uint64_t g0 = tile_index(A.sh, t, tid);
-    cplx wv[EPT], cur[EPT], nxt[EPT];
+    cplx wv[EPT];
     #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      wv[i] = make_double2(0.0, 0.0);
-      cur[i] = ld_stream(A.v[0] + g0 + off[i]);
-    }
-    // register double buffer: vector k+1 is in flight while vector k is accumulated
-    for (int k = 0; k < A.k; ++k) {
-      if (k + 1 < A.k) {
-        const cplx* vn = A.v[k + 1] + g0;
-        #pragma unroll
-        for (int i = 0; i < EPT; ++i) nxt[i] = ld_stream(vn + off[i]);
-      }
+    for (int i = 0; i < EPT; ++i) wv[i] = make_double2(0.0, 0.0);
+    int qstage = 0;
+    for (int k = 0; k < kv; ++k) {
+      cp_async_wait<1>();   // this item landed; the next one may still be in flight
+      const cplx* src = s + stage * TILE + tid;
       const double2 c = A.coef[k];
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
-        wv[i].x = fma(c.x, cur[i].x, fma(-c.y, cur[i].y, wv[i].x));
-        wv[i].y = fma(c.x, cur[i].y, fma(c.y, cur[i].x, wv[i].y));
-        cur[i] = nxt[i];
+        const cplx x = src[i * NT];
+        wv[i].x = fma(c.x, x.x, fma(-c.y, x.y, wv[i].x));
+        wv[i].y = fma(c.x, x.y, fma(c.y, x.x, wv[i].y));
       }
+      issue_next();         // into the stage consumed one item ago
+      qstage = stage;
+      stage = stage == RING - 1 ? 0 : stage + 1;
     }
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -1002,8 +1024,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
     if (A.qsweep) {
       DiagRow<NT, EPT> dr;
       if (has_diag) dr.setup(A.dg, A.sh, t, tid, nullptr);
+      cplx* sw = s + qstage * TILE;   // refilled only after the second barrier below
       #pragma unroll
-      for (int i = 0; i < EPT; ++i) s[tid + i * NT] = wv[i];
+      for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = wv[i];
       __syncthreads();
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
@@ -1026,7 +1049,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
         const double c = A.fl.coef[f];
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-          const cplx p = s[(tid + i * NT) ^ m];
+          const cplx p = sw[(tid + i * NT) ^ m];
           acc_q = fma(c, fma(wv[i].x, p.x, wv[i].y * p.y), acc_q);
         }
       }
@@ -1047,6 +1070,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
     }
   }
 
+  cp_async_wait<0>();
   double mine[2];
   mine[0] = block_sum<NT>(acc_n, red);
   mine[1] = block_sum<NT>(acc_q, red);
@@ -1327,7 +1351,7 @@ template <int TB>
 cudaError_t launch_combine_tb(const CombineArgs& args, cudaStream_t st) {
   constexpr int NT = combine_threads(TB);
   static int occ = 0;
-  return launch_persistent(combine_kernel<TB, NT>, args, args.sh.n_tiles, NT, (1 << TB) * sizeof(cplx), &occ, st);
+  return launch_persistent(combine_kernel<TB, NT>, args, args.sh.n_tiles, NT, 3 * (1 << TB) * sizeof(cplx), &occ, st);
 }
 
 }  // namespace

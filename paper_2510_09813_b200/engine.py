@@ -4,8 +4,10 @@ PyTorch is the plumbing here: it owns the device allocations (the Krylov slots)
 and the CUDA stream; every byte of arithmetic runs in ``_rsv.so``.
 
 HBM layout for N qubits (16 B per amplitude, 2^N amplitudes per vector):
-  slots[0 .. K]   Krylov vectors s_0..s_K (s_0 is the state), unnormalised
-  slots[K + 1]    work vector (partial H.v sums, then the next state)
+  slots[0 .. K-1] Krylov basis s_0..s_{K-1} (s_0 is the state), unnormalised
+  slots[K]        Lanczos iteration K-1's partial sums / residual (iteration j keeps its
+                  partial sums u in slot j+1 and turns them into s_{j+1} in place; the
+                  Krylov combination overwrites s_0 in place)
   dvec            optional 2^N float64 interaction diagonal (diag="vec" only)
 K is min(max_krylov_dim, what fits in free HBM); steps that would need more
 vectors are split exactly in time by the driver (rsv_capi.cu).
@@ -97,9 +99,9 @@ def slots_that_fit(n_qubits: int, max_krylov_dim: int, diag: str, device, budget
                    vector_cap=None) -> int:
     torch = _torch()
     slot_bytes = 16 << n_qubits
-    want = min(int(max_krylov_dim), KMAX_NATIVE) + 2
+    want = min(int(max_krylov_dim), KMAX_NATIVE) + 1
     if vector_cap is not None:
-        want = min(want, int(vector_cap) + 2)
+        want = min(want, int(vector_cap) + 1)
     free, _total = torch.cuda.mem_get_info(device)
     extra = (8 << n_qubits) if diag == "vec" else 0
     avail = free - RESERVE_BYTES - extra
@@ -121,7 +123,7 @@ class SvEngine(Context):
             need = (16 << self.n) * 3
             raise MemoryBudgetError(
                 f"state-vector workspace for N={self.n} needs at least {need:.3e} bytes of HBM "
-                "(state + one Krylov vector + work)", required_bytes=need, budget_bytes=memory_budget_bytes)
+                "(state + two Lanczos vectors)", required_bytes=need, budget_bytes=memory_budget_bytes)
         with torch.cuda.device(self.device):
             self.slots = [torch.empty(1 << self.n, dtype=torch.complex128, device=self.device)
                           for _ in range(nslots)]
@@ -132,7 +134,7 @@ class SvEngine(Context):
                 self.dvec = torch.empty(1 << self.n, dtype=torch.float64, device=self.device)
                 self.sync_stream()
                 nat.check(self.lib.rsv_bind_diag_vector(self.ctx, ctypes.c_void_p(self.dvec.data_ptr()), 1))
-        self.krylov_cap = nslots - 2
+        self.krylov_cap = nslots - 1
         self.masks = np.zeros(0, dtype=np.uint64)
         self.set_basis_state(0)
 
