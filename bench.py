@@ -221,6 +221,22 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def ncu_traffic(family, n, plan):
+    """DRAM bytes per launch of `family` from the committed ncu --set full summary (profiles/),
+    when it was captured for this N and pass plan; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_n29_summary.json")) as fh:
+            d = json.load(fh)
+    except Exception:
+        return None, None
+    if d.get("n") != n or d.get("plan", "plain") != plan:
+        return None, None
+    k = d.get("kernels", {}).get(family)
+    if not k or "traffic_bytes" not in k:
+        return None, None
+    return int(k["traffic_bytes"]), k.get("kernel")
+
+
 def alg_bytes_per_launch(family, n, k_avg, diag):
     """Algorithmic HBM bytes of one launch of a kernel family ('Roofline accounting').
 
@@ -232,7 +248,7 @@ def alg_bytes_per_launch(family, n, k_avg, diag):
     combine : read the k basis vectors, write psi ((k + 1) x 16 B)
     """
     amp = 2 ** n
-    if family in ("lo", "chunk"):
+    if family in ("lo", "chunk", "first"):
         prev_frac = (k_avg - 1.0) / k_avg if k_avg > 0 else 0.0
         return (32 + 16 * prev_frac + (8 if diag == "vec" else 0)) * amp
     if family in ("mid", "last"):
@@ -312,6 +328,8 @@ def run_ours(args):
     alg = alg_bytes_per_launch(fam, n, k_avg, args.diag)
     achieved = alg / (avg_launch_ms / 1e3) / 1e9
     kernel_launches = int(sum(v["launches"] for v in prof.values()))
+    plan_name = "chunk" if plan and plan[0].get("family") == "chunk" else "plain"
+    traffic, traffic_kernel = ncu_traffic(fam, n, plan_name) if args.diag == "fly" else (None, None)
     pass_ms = {f: round(v["ms"], 3) for f, v in prof.items()}
 
     # ---- e2e through the public API: host initial state in, host final state + occupations out
@@ -389,7 +407,10 @@ def run_ours(args):
             "kernel_ms": pass_ms,
             "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm_peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": None,
+                         "traffic": traffic,
+                         "traffic_source": ("profiles/r1_ncu_n29_summary.json (dram__bytes_read.sum + "
+                                            f"dram__bytes_write.sum of one {traffic_kernel} launch)"
+                                            if traffic else None),
                          "alg_bytes_per_launch": alg, "avg_launch_ms": avg_launch_ms},
             "gpu_launches": kernel_launches,
             "clocks": clocks,

@@ -258,6 +258,9 @@ cplx* slot(const rsv_context* c, int logical_index) {
 #ifndef RSV_DELEGATE_LOW
 #define RSV_DELEGATE_LOW 3
 #endif
+#ifndef RSV_LO_LAST
+#define RSV_LO_LAST 0
+#endif
 #ifndef RSV_LAST_TOP
 #define RSV_LAST_TOP 1
 #endif
@@ -359,6 +362,17 @@ void build_plan(rsv_context* c) {
     l.qubits.erase(l.qubits.begin(), l.qubits.begin() + kDelegateLow);
     for (int q = 0; q < kDelegateLow; ++q) m.qubits.push_back(q);
   }
+#if RSV_LO_LAST
+  // lo pass last: the q-sweep and the Krylov combination then run on contiguous tiles, the
+  // strided passes (top group first) carry no q-sweep
+  if (c->plan.size() >= 2) {
+    std::vector<PassPlan> hi(c->plan.begin() + 1, c->plan.end());
+    std::vector<PassPlan> order;
+    for (size_t i = hi.size(); i-- > 0;) order.push_back(hi[i]);
+    order.push_back(c->plan[0]);
+    c->plan = order;
+  }
+#endif
 }
 
 rsv::FlipSet flips_for(const PassPlan& p, const double* omegas, int nthreads) {
@@ -396,7 +410,7 @@ rsv::DiagArgs diag_for(const rsv_context* c, const PassPlan& p, const double* de
 }
 
 int ensure_dl(rsv_context* c, const double* deltas) {
-  const int alo = c->plan[0].sh.a;
+  const int alo = std::min(c->n, rsv::kLoBits);   // the lo tile (wherever it sits in the plan)
   std::vector<double> key(deltas, deltas + c->n);
   if (c->dl_valid && key == c->dl_key) return RSV_OK;
   const bool fly = c->diag_mode == RSV_DIAG_FLY;

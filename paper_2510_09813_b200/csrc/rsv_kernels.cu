@@ -16,6 +16,10 @@
 #ifndef RSV_TMA
 #define RSV_TMA 1
 #endif
+// rotating tile buffers: the elementwise operand is prefetched one tile ahead too (pass_kernel_rot)
+#ifndef RSV_ROT
+#define RSV_ROT 1
+#endif
 #ifndef RSV_EIN_REGS
 #define RSV_EIN_REGS 0
 #endif
@@ -627,6 +631,228 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
       }
       fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
     }
+  }
+  acc_a *= xs;
+
+  if (KIND == PASS_LAST_APPLY) return;
+  double mine[3];
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = block_sum<NT>(acc_n, red);
+  mine[2] = block_sum<NT>(acc_q, red);
+  double tot[3];
+  if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
+  if (threadIdx.x != 0) return;
+  double* scw = A.sc;
+  if (KIND == PASS_FIRST) {
+    scw[SC_AP + A.j] = tot[0];
+  } else if (KIND == PASS_MID) {
+    scw[SC_AP + A.j] += tot[0];
+  } else {
+    const double nrm2 = tot[1];
+    const double beta = sqrt(nrm2);
+    scw[SC_AL + A.j] = alpha;
+    scw[SC_BE + A.j] = beta;
+    scw[SC_SG + A.j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
+    scw[SC_Q + A.j + 1] = nrm2 > 0.0 ? tot[2] / nrm2 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- bit-group pass, rotating buffers
+// Same arithmetic as pass_kernel_tma, but both operands are prefetched: three tile buffers rotate
+// through the roles "x of tile it", "operand of tile it" and "x of tile it+1". Buffer it%3 holds
+// x(it); once every thread is past the flips (barrier B) it receives the operand of tile it+1, so
+// that load has a whole epilogue plus the next tile's flips to land; the operand buffer of tile it
+// receives x(it+2) after the next tile barrier (A). Cost: one more CTA barrier per tile.
+template <int TB, int KIND, int NT, bool DIAG>
+__global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kernel_rot(const __grid_constant__ PassArgs A) {
+  constexpr int TILE = 1 << TB;
+  constexpr int EPT = TILE / NT;
+  constexpr int RB = RegBits<EPT>::value;
+  constexpr bool LANCZOS = KIND == PASS_LAST_LANCZOS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  cplx* buf = reinterpret_cast<cplx*>(smem_al);              // [3][TILE]
+  double* rows = reinterpret_cast<double*>(buf + 3 * TILE);  // [3][16] tile-table rows (ride with x)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 48);   // one mbarrier per buffer
+  __shared__ double red[32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* sc = A.sc;
+  const double xs = sc[A.x_scale_slot];
+  double alpha = 0.0;
+  if (LANCZOS) alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
+  const bool has_e = A.ein != nullptr;
+  const double ecoef = A.ein_is_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 1.0;
+  double rc[RB > 0 ? RB : 1];
+  #pragma unroll
+  for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
+  const double axs = alpha * xs;
+  double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
+  const uint64_t S = elem_offset(A.sh, NT);
+  const uint64_t ntiles = A.sh.n_tiles;
+  const uint64_t G = gridDim.x;
+
+  const int R = (1 << A.sh.a) < 32 ? (1 << A.sh.a) : (NT < 32 ? NT : 32);
+  const int RUNS = (NT < 32 ? NT : 32) / R;
+  const unsigned x_bytes = TILE * sizeof(cplx) + (DIAG ? 112u : 0u);
+  auto issue = [&](const cplx* base, const CUtensorMap* map, uint64_t tt, cplx* dst, uint64_t* bar) {
+    if (A.load == LOAD_CONTIG) {
+      if (tid == 0) bulk_g2s(dst, base + tile_index(A.sh, tt, 0), TILE * sizeof(cplx), bar);
+      return;
+    }
+    if (A.load == LOAD_TENSOR) {
+      if (tid == 0) {
+        const int m = A.sh.p - A.sh.a;
+        tma_load_5d(dst, map, 0, (int)(tt & ((1ull << m) - 1ull)), 0, 0, (int)(tt >> m), bar);
+      }
+      return;
+    }
+    if (lane < RUNS) {
+      const uint32_t e0 = (uint32_t)(warp * 32 + lane * R);
+      const cplx* src = base + tile_index(A.sh, tt, e0);
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) bulk_g2s(dst + e0 + i * NT, src + i * S, R * sizeof(cplx), bar);
+    }
+  };
+  auto issue_x = [&](uint64_t tt, int b) {
+    issue(A.x, &A.tm_x, tt, buf + b * TILE, &bars[b]);
+    if (DIAG && tid == 0) bulk_g2s(rows + b * 16, A.dg.gc + tt * kGcStride, 112, &bars[b]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  unsigned phase = 0u;   // bit b: parity of buffer b's next completion
+  const uint64_t t0 = blockIdx.x;
+  if (t0 < ntiles) {   // prologue: x(0) -> buffer 0, operand(0) -> buffer 2
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bars[0], x_bytes);
+      if (has_e) mbar_arrive_expect_tx(&bars[2], TILE * sizeof(cplx));
+    }
+    __syncthreads();
+    issue_x(t0, 0);
+    if (has_e) issue(A.ein, &A.tm_e, t0, buf + 2 * TILE, &bars[2]);
+  }
+  int bx = 0;   // buffer of x(it); the operand of tile it sits in (bx + 2) % 3
+  for (uint64_t t = t0; t < ntiles; t += G) {
+    const int be = bx == 0 ? 2 : bx - 1;
+    const int bn = bx == 2 ? 0 : bx + 1;
+    const uint64_t g0 = tile_index(A.sh, t, tid);
+    const uint64_t tn = t + G;
+    if (tid == 0 && tn < ntiles) mbar_arrive_expect_tx(&bars[bn], x_bytes);
+    mbar_wait(&bars[bx], (phase >> bx) & 1u);
+    phase ^= 1u << bx;
+    __syncthreads();   // (A) everyone is past tile it-1: its operand buffer (= bn) is free
+    if (tn < ntiles) issue_x(tn, bn);
+    const cplx* s = buf + bx * TILE;
+    DiagRow<NT, EPT> dr;
+    if (DIAG) dr.setup(A.dg, A.sh, t, tid, rows + bx * 16);
+
+    cplx xv[EPT], ac[EPT];
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      xv[i] = s[tid + i * NT];
+      ac[i] = make_double2(0.0, 0.0);
+    }
+    #pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        ac[i].x = fma(rc[b], xv[i ^ (1 << b)].x, ac[i].x);
+        ac[i].y = fma(rc[b], xv[i ^ (1 << b)].y, ac[i].y);
+      }
+    }
+    for (int f = 0; f < A.fl.count; ++f) {
+      const cplx* ps = s + (tid ^ A.fl.mask[f]);
+      const double c = A.fl.coef[f] * xs;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const cplx p = ps[i * NT];
+        ac[i].x = fma(c, p.x, ac[i].x);
+        ac[i].y = fma(c, p.y, ac[i].y);
+      }
+    }
+    if (DIAG) {
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        double d = dr.d[i];
+        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+        d *= xs;
+        ac[i].x = fma(d, xv[i].x, ac[i].x);
+        ac[i].y = fma(d, xv[i].y, ac[i].y);
+      }
+    }
+    if (has_e && tn < ntiles) {
+      if (tid == 0) mbar_arrive_expect_tx(&bars[bx], TILE * sizeof(cplx));
+      __syncthreads();   // (B) everyone is past the flips on x(it): its buffer takes operand(it+1)
+      issue(A.ein, &A.tm_e, tn, buf + bx * TILE, &bars[bx]);
+    }
+    const cplx* eb = buf + be * TILE;
+    if (has_e) {
+      mbar_wait(&bars[be], (phase >> be) & 1u);
+      phase ^= 1u << be;
+    }
+    cplx* po = A.out + g0;
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      double cr = ac[i].x, ci = ac[i].y;
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
+      if (has_e) {
+        const cplx u = eb[tid + i * NT];
+        cr = fma(ecoef, u.x, cr);
+        ci = fma(ecoef, u.y, ci);
+      }
+      if (LANCZOS) {
+        cr = fma(-axs, xv[i].x, cr);
+        ci = fma(-axs, xv[i].y, ci);
+        acc_n = fma(cr, cr, fma(ci, ci, acc_n));
+      }
+      ac[i] = make_double2(cr, ci);
+      st_stream(po + i * S, ac[i]);
+    }
+
+    if (LANCZOS && A.qsweep) {
+      // w goes to the operand buffer of this tile (refilled only after the next barrier A);
+      // without an operand that buffer is idle
+      cplx* sw = buf + be * TILE;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
+      __syncthreads();
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        double hr = 0.0, hi = 0.0;
+        #pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          if ((i >> b) & 1) continue;
+          hr = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].x, hr);
+          hi = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].y, hi);
+        }
+        if (DIAG) {
+          double d = dr.d[i];
+          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+          hr = fma(d, ac[i].x, hr);
+          hi = fma(d, ac[i].y, hi);
+        }
+        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
+      }
+      for (int f = 0; f < A.fl.count; ++f) {
+        const int m = A.fl.mask[f];
+        if (tid & m) continue;
+        const cplx* ps = sw + (tid ^ m);
+        const double c2 = 2.0 * A.fl.coef[f];
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const cplx p = ps[i * NT];
+          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
+        }
+      }
+      fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
+    }
+    bx = bn;
   }
   acc_a *= xs;
 
@@ -1300,6 +1526,16 @@ cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, in
 template <int TB, int KIND, bool DIAG>
 cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   constexpr int NT = pass_threads(TB);
+#if RSV_TMA && RSV_ROT
+  // measured at N=26/29: the prefetched operand pays off in the last pass (its q-sweep leaves
+  // less time to hide the operand load); the lo/mid passes are faster without the extra barrier
+  if constexpr (TB >= 3 && KIND == PASS_LAST_LANCZOS) {
+    static int occ_rot = 0;
+    constexpr size_t smem_rot = 3 * (1 << TB) * sizeof(cplx) + 48 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+    return launch_persistent(pass_kernel_rot<TB, KIND, NT, DIAG>, args, args.sh.n_tiles, NT, smem_rot, &occ_rot,
+                             st);
+  }
+#endif
 #if RSV_TMA
   if constexpr (TB >= 3) {
     static int occ_tma = 0;
@@ -1319,8 +1555,6 @@ cudaError_t launch_pass_tbk(const PassArgs& args, cudaStream_t st) {
   // the diagonal lives in the lo pass only: the middle passes never carry it
   if constexpr (KIND == PASS_MID) {
     return launch_pass_tbkd<TB, KIND, false>(args, st);
-  } else if constexpr (KIND == PASS_FIRST) {
-    return launch_pass_tbkd<TB, KIND, true>(args, st);   // the first pass is always the lo pass
   } else {
     if (args.dg.mode != DIAG_NONE) return launch_pass_tbkd<TB, KIND, true>(args, st);
     return launch_pass_tbkd<TB, KIND, false>(args, st);

@@ -212,6 +212,7 @@ class SvEngine(Context):
         ms = (ctypes.c_double * 4)()
         cnt = (ctypes.c_longlong * 4)()
         nat.check(self.lib.rsv_get_profile(self.ctx, ms, cnt))
-        first = "chunk" if self.pass_plan()[0]["family"] == "chunk" else "lo"
+        p0 = self.pass_plan()[0]
+        first = "chunk" if p0["family"] == "chunk" else ("lo" if p0["lo"] else "first")
         names = (first, "mid", "last", "combine")
         return {names[i]: {"ms": ms[i], "launches": cnt[i]} for i in range(4)}
