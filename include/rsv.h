@@ -112,6 +112,27 @@ int rsv_scale(rsv_context* ctx, void* y, const void* x, double a_re, double a_im
 
 /* Introspection / measurement support. */
 int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass: a, p, g, lo, family, chunk_gm] */
+/* Sharding by the top log2(P) qubits (north-star row e; paper_2510_09813_b200/sharding.py). The context
+ * is created for the LOCAL qubits (n - log2 P) with the local interaction block; per step the host passes
+ * the shard's effective detunings as `deltas` of rsv_expm_step and the rest through rsv_set_shard_step.
+ * The driver calls `comm` synchronously (its stream idle):
+ *   RSV_COMM_ALLREDUCE       host[0..count) summed over all ranks, in place;
+ *   RSV_COMM_EXCHANGE_START  start sending bound slot `slot` to rank `peer` and receiving the peer's copy into
+ *                            the exchange buffer (may run concurrently with the local passes);
+ *   RSV_COMM_EXCHANGE_WAIT   complete that exchange.
+ * Reference counterpart: none (the reference is single-process, rydsim/sv.py:80). */
+#define RSV_COMM_ALLREDUCE 1
+#define RSV_COMM_EXCHANGE_START 2
+#define RSV_COMM_EXCHANGE_WAIT 3
+typedef int (*rsv_comm_fn)(void* user, int op, int slot, int peer, double* host, int count);
+int rsv_set_shard(rsv_context* ctx, rsv_comm_fn comm, void* user, void* exchange_buffer);
+/* This step's constant energy of the shard's global bits (and the next step's), and per global qubit
+ * Omega_g/2 (0 = no flip) with the partner rank. */
+int rsv_set_shard_step(rsv_context* ctx, double offset, double next_offset, int n_global, const double* coef,
+                       const int* peer);
+/* This shard's share of ||psi||^2 from the last Krylov combination / measurement. */
+int rsv_shard_local_norm_sq(rsv_context* ctx, double* out);
+
 /* Pass-plan override (tests / tuning): chunk_group_bits -1 = auto (chunk pass at N >= 22), 0 = plain
  * bit-group passes, 3..9 = force the L2-resident chunk pass over bits [0, 12 + g); chunk_lag = M tiles
  * handed out ahead of the first L tile (-1 = auto, 1.5 chunks). No reference counterpart: the reference

@@ -43,6 +43,13 @@ class KrylovReportC(ctypes.Structure):
     ]
 
 
+# rsv_comm_fn (include/rsv.h): int (*)(void* user, int op, int slot, int peer, double* host, int count)
+COMM_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                           ctypes.POINTER(ctypes.c_double), ctypes.c_int)
+RSV_COMM_ALLREDUCE = 1
+RSV_COMM_EXCHANGE_START = 2
+RSV_COMM_EXCHANGE_WAIT = 3
+
 # name -> (restype, argtypes); exactly the symbols declared in include/rsv.h
 SIGNATURES = {
     "rsv_version": (ctypes.c_int, []),
@@ -78,6 +85,10 @@ SIGNATURES = {
                                  ctypes.c_double, ctypes.c_uint64]),
     "rsv_pass_plan": (ctypes.c_int, [ctypes.c_void_p, c_int_p, ctypes.c_int]),
     "rsv_set_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]),
+    "rsv_set_shard": (ctypes.c_int, [ctypes.c_void_p, COMM_FN, ctypes.c_void_p, ctypes.c_void_p]),
+    "rsv_set_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                          c_double_p, c_int_p]),
+    "rsv_shard_local_norm_sq": (ctypes.c_int, [ctypes.c_void_p, c_double_p]),
     "rsv_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_get_profile": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_ll_p]),
     "rsv_reset_profile": (ctypes.c_int, [ctypes.c_void_p]),

@@ -216,6 +216,16 @@ struct rsv_context {
   std::vector<void*> phys;        // bound slots
   std::vector<int> logical;       // logical slot -> physical; logical 0..K = Krylov s_j, K+1 = work
   std::vector<PassPlan> plan;
+  // sharding by the top qubits (row e; sharding.py): this context holds one shard's local qubits
+  bool sharded = false;
+  rsv_comm_fn comm = nullptr;
+  void* comm_user = nullptr;
+  cplx* xbuf = nullptr;             // exchange buffer (the partner shard's copy of s_j)
+  double offset = 0.0, next_offset = 0.0;   // constant energy of this shard's global bits
+  std::vector<double> gcoef;        // Omega_g / 2 of each global qubit this step (0: no flip)
+  std::vector<int> gpeer;           // partner rank of each global qubit
+  double n0sq_global = 0.0;         // ||psi||^2 over all shards from the last combination
+  double local_n0sq = 0.0;          // this shard's share of it
   int plan_gm = -1;               // chunk group bits: -1 auto, 0 off, 3..9 forced (rsv_set_plan)
   long long plan_lag = -1;        // chunk scheduler lag in M tiles (-1 auto)
   unsigned long long* d_ticket = nullptr;
@@ -409,12 +419,13 @@ rsv::DiagArgs diag_for(const rsv_context* c, const PassPlan& p, const double* de
   return d;
 }
 
-int ensure_dl(rsv_context* c, const double* deltas) {
+int ensure_dl(rsv_context* c, const double* deltas, double offset = 0.0) {
   const int alo = std::min(c->n, rsv::kLoBits);   // the lo tile (wherever it sits in the plan)
   std::vector<double> key(deltas, deltas + c->n);
+  key.push_back(offset);
   if (c->dl_valid && key == c->dl_key) return RSV_OK;
   const bool fly = c->diag_mode == RSV_DIAG_FLY;
-  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, deltas, fly ? 1 : 0, c->d_dl, c->st));
+  CUDA_TRY(rsv::launch_build_dl(alo, c->n, c->d_u, deltas, fly ? 1 : 0, offset, c->d_dl, c->st));
   CUDA_TRY(rsv::launch_tile_base(alo, c->n, fly ? 1 : 0, deltas, c->d_gc, c->st));
   c->dl_key = key;
   c->dl_valid = true;
@@ -422,11 +433,14 @@ int ensure_dl(rsv_context* c, const double* deltas) {
 }
 
 // Key of everything the prepared q_0 depends on: last-pass drives (+ detunings if it holds the diagonal).
-std::vector<double> prep_key_for(const rsv_context* c, const double* omegas, const double* deltas) {
+std::vector<double> prep_key_for(const rsv_context* c, const double* omegas, const double* deltas, double off) {
   const PassPlan& last = c->plan.back();
   std::vector<double> k;
   for (int q : last.qubits) k.push_back(omegas[q]);
-  if (last.lo) k.insert(k.end(), deltas, deltas + c->n);
+  if (last.lo) {
+    k.insert(k.end(), deltas, deltas + c->n);
+    k.push_back(off);
+  }
   return k;
 }
 
@@ -464,9 +478,109 @@ int family_of(size_t pass_index, size_t npass) {
   return pass_index == 0 ? 0 : 1;
 }
 
+// ---- sharded runs: the host side of the all-reduces and the global-qubit exchanges
+int comm_call(rsv_context* c, int op, int slot_index, int peer, double* host, int count) {
+  const int rc = c->comm(c->comm_user, op, slot_index, peer, host, count);
+  if (rc != 0) return fail(RSV_ERR_CUDA, "shard communication callback failed (op %d, rc %d)", op, rc);
+  return RSV_OK;
+}
+
+// After a raw combination: all-reduce ||psi||^2, <psi|A_last|psi> and the mask sums, finish the scalars.
+int shard_finish_combine(rsv_context* c, int nmask) {
+  double* h = c->h_pin;
+  CUDA_TRY(cudaMemcpyAsync(h + rsv::SC_N0SQ, c->d_sc + rsv::SC_N0SQ, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaMemcpyAsync(h + rsv::SC_Q, c->d_sc + rsv::SC_Q, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  if (nmask > 0)
+    CUDA_TRY(cudaMemcpyAsync(h + rsv::SC_OBS, c->d_sc + rsv::SC_OBS, sizeof(double) * nmask, cudaMemcpyDeviceToHost,
+                             c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  std::vector<double> buf(2 + nmask);
+  buf[0] = h[rsv::SC_N0SQ];
+  buf[1] = h[rsv::SC_Q];
+  for (int m = 0; m < nmask; ++m) buf[2 + m] = h[rsv::SC_OBS + m];
+  c->local_n0sq = buf[0];
+  int rc = comm_call(c, RSV_COMM_ALLREDUCE, -1, -1, buf.data(), (int)buf.size());
+  if (rc) return rc;
+  const double nsq = buf[0];
+  c->n0sq_global = nsq;
+  double fin[3] = {nsq, nsq > 0.0 ? 1.0 / std::sqrt(nsq) : 0.0, nsq > 0.0 ? buf[1] / nsq : 0.0};
+  h[rsv::SC_N0SQ] = nsq;
+  for (int m = 0; m < nmask; ++m) h[rsv::SC_OBS + m] = buf[2 + m];
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_N0SQ, &fin[0], sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_SG, &fin[1], sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_Q, &fin[2], sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (nmask > 0) {
+    CUDA_TRY(cudaEventRecord(c->obs_event, c->st));
+    c->obs_pending = true;
+    c->obs_count = nmask;
+  }
+  return RSV_OK;
+}
+
+// Before the last pass of iteration j: the global-qubit flips (partner shard's s_j, exchanged by the
+// host) are added to the partial sums u (slot j+1), and alpha's partial share is all-reduced.
+// The first exchange was started before the local passes (overlapped with them).
+int shard_before_last(rsv_context* c, int j, double sigma, bool started) {
+  double add = 0.0;
+  const uint64_t nloc = 1ull << c->n;
+  bool first = true;
+  for (size_t g = 0; g < c->gcoef.size(); ++g) {
+    if (c->gcoef[g] == 0.0) continue;
+    int rc;
+    if (!(first && started)) {
+      CUDA_TRY(cudaStreamSynchronize(c->st));
+      rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[j], c->gpeer[g], nullptr, 0);
+      if (rc) return rc;
+    }
+    first = false;
+    rc = comm_call(c, RSV_COMM_EXCHANGE_WAIT, c->logical[j], c->gpeer[g], nullptr, 0);
+    if (rc) return rc;
+    const double cs = c->gcoef[g] * sigma;
+    CUDA_TRY(rsv::launch_global_flip(slot(c, j + 1), c->xbuf, slot(c, j), cs, nloc, c->d_part, c->d_counter,
+                                     c->d_sc + rsv::SC_GF, c->st));
+    double dot = 0.0;
+    CUDA_TRY(cudaMemcpyAsync(&c->h_pin[rsv::SC_GF], c->d_sc + rsv::SC_GF, sizeof(double), cudaMemcpyDeviceToHost,
+                             c->st));
+    CUDA_TRY(cudaStreamSynchronize(c->st));   // the exchange buffer is free again
+    dot = c->h_pin[rsv::SC_GF];
+    add += cs * sigma * dot;
+  }
+  CUDA_TRY(cudaMemcpyAsync(&c->h_pin[rsv::SC_AP + j], c->d_sc + rsv::SC_AP + j, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  double ap = c->h_pin[rsv::SC_AP + j] + add;
+  int rc = comm_call(c, RSV_COMM_ALLREDUCE, -1, -1, &ap, 1);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_AP + j, &ap, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return RSV_OK;
+}
+
+// After the (raw) last pass of iteration j: all-reduce ||w_j||^2 and <w_j|A_last|w_j>, write back
+// beta_j, sigma_{j+1}, q_{j+1}.
+int shard_finish_iteration(rsv_context* c, int j) {
+  double* h = c->h_pin;
+  CUDA_TRY(cudaMemcpyAsync(h + rsv::SC_BE + j, c->d_sc + rsv::SC_BE + j, sizeof(double), cudaMemcpyDeviceToHost,
+                           c->st));
+  CUDA_TRY(cudaMemcpyAsync(h + rsv::SC_Q + j + 1, c->d_sc + rsv::SC_Q + j + 1, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  double buf[2] = {h[rsv::SC_BE + j], h[rsv::SC_Q + j + 1]};
+  int rc = comm_call(c, RSV_COMM_ALLREDUCE, -1, -1, buf, 2);
+  if (rc) return rc;
+  const double nrm2 = buf[0], beta = std::sqrt(std::max(0.0, nrm2));
+  const double sg = beta > 0.0 ? 1.0 / beta : 0.0, q = nrm2 > 0.0 ? buf[1] / nrm2 : 0.0;
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_BE + j, &beta, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_SG + j + 1, &sg, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_Q + j + 1, &q, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return RSV_OK;
+}
+
 // Krylov combination (also "prepare": k = 1, coefficient 1, in place).
 int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, const double* q_omegas,
-                const double* q_deltas, int observe) {
+                const double* q_deltas, int observe, double q_offset = 0.0) {
   rsv::CombineArgs A{};
   const PassPlan& last = c->plan.back();
   A.sh = last.sh;
@@ -475,7 +589,7 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
     A.fl = flips_for(last, q_omegas, rsv::combine_threads(last.sh.a + last.sh.g));
     A.dg = diag_for(c, last, q_deltas);
     if (last.lo) {
-      int rc = ensure_dl(c, q_deltas);
+      int rc = ensure_dl(c, q_deltas, q_offset);
       if (rc) return rc;
     }
   } else {
@@ -494,9 +608,11 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
   A.sc = c->d_sc;
   A.part = c->d_part;
   A.counter = c->d_counter;
+  A.raw = c->sharded ? 1 : 0;
   prof_begin(c, 3);
   CUDA_TRY(rsv::launch_combine(A, c->st));
   prof_end(c);
+  if (c->sharded) return shard_finish_combine(c, A.nmask);
   if (A.nmask > 0) {
     CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_OBS, c->d_sc + rsv::SC_OBS, sizeof(double) * A.nmask,
                              cudaMemcpyDeviceToHost, c->st));
@@ -511,9 +627,9 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
 
 int prepare(rsv_context* c, const double* omegas, const double* deltas) {
   std::vector<zc> one(1, zc(1.0, 0.0));
-  int rc = run_combine(c, 1, one, slot(c, 0), omegas, deltas, 0);
+  int rc = run_combine(c, 1, one, slot(c, 0), omegas, deltas, 0, c->offset);
   if (rc) return rc;
-  c->prep_key = prep_key_for(c, omegas, deltas);
+  c->prep_key = prep_key_for(c, omegas, deltas, c->offset);
   c->prep_valid = true;
   return RSV_OK;
 }
@@ -557,10 +673,37 @@ int launch_chunk_pass(rsv_context* c, const PassPlan& p, const double* omegas, c
   return RSV_OK;
 }
 
-int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const double* deltas) {
+int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const double* deltas, double sigma,
+                             double prev_coef) {
   const size_t np = c->plan.size();
+  // sharded: start the first global-qubit exchange of s_j so it overlaps the local passes
+  bool started = false;
+  if (c->sharded) {
+    for (size_t g = 0; g < c->gcoef.size(); ++g) {
+      if (c->gcoef[g] == 0.0) continue;
+      CUDA_TRY(cudaStreamSynchronize(c->st));
+      int rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[j], c->gpeer[g], nullptr, 0);
+      if (rc) return rc;
+      started = true;
+      break;
+    }
+  }
   for (size_t pi = 0; pi < np; ++pi) {
     const PassPlan& p = c->plan[pi];
+    if (c->sharded && pi + 1 == np) {
+      if (np == 1) {
+        // a single pass has no partial sums to add the global flips to: seed u = -beta' s_{j-1}
+        // (its elementwise operand) in slot j+1 and let the pass read u instead
+        const uint64_t nloc = 1ull << c->n;
+        if (j > 0) {
+          CUDA_TRY(rsv::launch_scale(slot(c, j + 1), slot(c, j - 1), make_double2(prev_coef, 0.0), nloc, 0, c->st));
+        } else {
+          CUDA_TRY(cudaMemsetAsync(slot(c, j + 1), 0, sizeof(cplx) * nloc, c->st));
+        }
+      }
+      int rc = shard_before_last(c, j, sigma, started);
+      if (rc) return rc;
+    }
     if (p.chunk) {
       int rc = launch_chunk_pass(c, p, omegas, deltas, slot(c, j), rsv::SC_SG + j, j > 0 ? slot(c, j - 1) : nullptr,
                                  slot(c, j + 1), j);
@@ -583,12 +726,17 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     if (pi == 0) {
       A.ein = j > 0 ? slot(c, j - 1) : nullptr;
       A.ein_is_prev = 1;
+      if (c->sharded && np == 1) {
+        A.ein = slot(c, j + 1);
+        A.ein_is_prev = 0;
+      }
     } else {
       A.ein = slot(c, j + 1);
       A.ein_is_prev = 0;
     }
     A.out = slot(c, j + 1);   // u in place, then s_{j+1}
     A.qsweep = last ? 1 : 0;
+    A.raw = (last && c->sharded) ? 1 : 0;
     set_tile_load(A);
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
@@ -604,11 +752,18 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
                 double norm_eps, const double* q_omegas, const double* q_deltas, bool last_run, int observe,
                 rsv_krylov_report* rep, bool first_run, double* advanced, bool* zero_vector) {
   *zero_vector = false;
-  if (!c->prep_valid || c->prep_key != prep_key_for(c, omegas, deltas)) {
+  bool need_prep = !c->prep_valid || c->prep_key != prep_key_for(c, omegas, deltas, c->offset);
+  if (c->sharded) {   // collectives must be entered by every shard: decide together
+    double flag = need_prep ? 1.0 : 0.0;
+    int rc = comm_call(c, RSV_COMM_ALLREDUCE, -1, -1, &flag, 1);
+    if (rc) return rc;
+    need_prep = flag > 0.0;
+  }
+  if (need_prep) {
     int rc = prepare(c, omegas, deltas);
     if (rc) return rc;
   }
-  int rc = ensure_dl(c, deltas);
+  int rc = ensure_dl(c, deltas, c->offset);
   if (rc) return rc;
   CUDA_TRY(cudaMemsetAsync(c->d_sc + rsv::SC_AP, 0, sizeof(double) * 128, c->st));
 
@@ -620,8 +775,21 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
   bool converged = false;
   int k = 0;
   for (int j = 0;; ++j) {
-    rc = launch_lanczos_iteration(c, j, omegas, deltas);
+    const double sigma = j == 0 ? (c->n0sq_global > 0.0 ? 1.0 / std::sqrt(c->n0sq_global) : 0.0)
+                                : (betas.back() > 0.0 ? 1.0 / betas.back() : 0.0);
+    // -beta_{j-1} sigma_{j-1}: the coefficient of s_{j-1} in iteration j (sharded single-pass plans)
+    double prev_coef = 0.0;
+    if (j > 0) {
+      const double sg_prev = j == 1 ? (c->n0sq_global > 0.0 ? 1.0 / std::sqrt(c->n0sq_global) : 0.0)
+                                    : (betas[j - 2] > 0.0 ? 1.0 / betas[j - 2] : 0.0);
+      prev_coef = -betas[j - 1] * sg_prev;
+    }
+    rc = launch_lanczos_iteration(c, j, omegas, deltas, sigma, prev_coef);
     if (rc) return rc;
+    if (c->sharded) {
+      rc = shard_finish_iteration(c, j);
+      if (rc) return rc;
+    }
     rep->matvecs += 1;
     CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_AL + j, c->d_sc + rsv::SC_AL + j, sizeof(double),
                              cudaMemcpyDeviceToHost, c->st));
@@ -699,10 +867,11 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
   const double* qo = more ? omegas : q_omegas;
   const double* qd = more ? deltas : q_deltas;
   // elementwise, so in place: every amplitude of s_0 is read before it is overwritten
-  rc = run_combine(c, k, coef, slot(c, 0), qo, qd, (!more && last_run && observe) ? 1 : 0);
+  rc = run_combine(c, k, coef, slot(c, 0), qo, qd, (!more && last_run && observe) ? 1 : 0,
+                   more ? c->offset : c->next_offset);
   if (rc) return rc;
   if (qo != nullptr) {
-    c->prep_key = prep_key_for(c, qo, qd);
+    c->prep_key = prep_key_for(c, qo, qd, more ? c->offset : c->next_offset);
     c->prep_valid = true;
   } else {
     c->prep_valid = false;
@@ -876,6 +1045,7 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     return fail(RSV_ERR_STATE, "diag_mode VEC needs rsv_bind_diag_vector first");
   const size_t np = c->plan.size();
   if (np > 1 && psi == out) return fail(RSV_ERR_ARG, "psi and out must not alias for N > %d", rsv::kLoBits);
+  if (c->sharded) return fail(RSV_ERR_STATE, "rsv_apply_hamiltonian applies the local operator only: unset the shard");
   int rc = ensure_dl(c, deltas);
   if (rc) return rc;
   for (size_t pi = 0; pi < np; ++pi) {
@@ -1057,6 +1227,43 @@ int rsv_pass_plan(rsv_context* c, int* out, int max_ints) {
     out[5 + 6 * i] = family_of(i, np);
     out[6 + 6 * i] = c->plan[i].chunk ? c->plan[i].gm : 0;
   }
+  return RSV_OK;
+}
+
+int rsv_set_shard(rsv_context* c, rsv_comm_fn comm, void* user, void* exchange_buffer) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (comm == nullptr) {
+    c->sharded = false;
+    c->comm = nullptr;
+    c->xbuf = nullptr;
+    return RSV_OK;
+  }
+  if (exchange_buffer == nullptr || (reinterpret_cast<uintptr_t>(exchange_buffer) & 15u))
+    return fail(RSV_ERR_ARG, "exchange buffer is NULL or not 16-byte aligned");
+  c->sharded = true;
+  c->comm = comm;
+  c->comm_user = user;
+  c->xbuf = reinterpret_cast<cplx*>(exchange_buffer);
+  c->prep_valid = false;
+  return RSV_OK;
+}
+
+int rsv_set_shard_step(rsv_context* c, double offset, double next_offset, int n_global, const double* coef,
+                       const int* peer) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (!c->sharded) return fail(RSV_ERR_STATE, "rsv_set_shard_step needs rsv_set_shard first");
+  if (n_global < 0 || n_global > 16 || (n_global > 0 && (coef == nullptr || peer == nullptr)))
+    return fail(RSV_ERR_ARG, "bad global-qubit list (%d entries)", n_global);
+  c->offset = offset;   // enters the prepared-q_0 key (prep_key_for) when the last pass holds the diagonal
+  c->next_offset = next_offset;
+  c->gcoef.assign(coef, coef + n_global);
+  c->gpeer.assign(peer, peer + n_global);
+  return RSV_OK;
+}
+
+int rsv_shard_local_norm_sq(rsv_context* c, double* out) {
+  if (!c || !out) return fail(RSV_ERR_ARG, "NULL argument");
+  *out = c->local_n0sq;
   return RSV_OK;
 }
 

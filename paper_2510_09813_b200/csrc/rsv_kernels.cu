@@ -158,6 +158,22 @@ struct Log2 {
   static constexpr int value = N <= 1 ? 0 : 1 + Log2<N / 2>::value;
 };
 
+// Last pass of Lanczos iteration j: alpha_j, beta_j, sigma_{j+1}, q_{j+1} from the grid sums
+// ||w||^2 and <w|A_last|w>. Sharded runs (raw) store the local sums (beta slot = ||w||^2, q slot =
+// <w|A|w>); the host all-reduces them and writes the scalars back (rsv_capi.cu, shard_finish_iteration).
+__device__ __forceinline__ void lanczos_scalars(double* scw, int j, int raw, double alpha, double nrm2, double qraw) {
+  scw[SC_AL + j] = alpha;
+  if (raw) {
+    scw[SC_BE + j] = nrm2;
+    scw[SC_Q + j + 1] = qraw;
+    return;
+  }
+  const double beta = sqrt(nrm2);
+  scw[SC_BE + j] = beta;
+  scw[SC_SG + j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
+  scw[SC_Q + j + 1] = nrm2 > 0.0 ? qraw / nrm2 : 0.0;
+}
+
 // ---------------------------------------------------------------- on-the-fly diagonal
 // For the lo tile (bits [0, a) contiguous, tile t = bits a..n-1):
 //   d(b) = dl[e] + hh[t] - sum_{j>=a} delta_j bit_j(t) + sum_{i<a} bit_i(e) gc[t][i]
@@ -424,13 +440,8 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
     scw[SC_AP + A.j] = tot[0];
   } else if (KIND == PASS_MID) {
     scw[SC_AP + A.j] += tot[0];
-  } else {  // LAST_LANCZOS
-    const double nrm2 = tot[1];
-    const double beta = sqrt(nrm2);
-    scw[SC_AL + A.j] = alpha;
-    scw[SC_BE + A.j] = beta;
-    scw[SC_SG + A.j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
-    scw[SC_Q + A.j + 1] = nrm2 > 0.0 ? tot[2] / nrm2 : 0.0;
+  } else {
+    lanczos_scalars(scw, A.j, A.raw, alpha, tot[1], tot[2]);
   }
 }
 
@@ -648,12 +659,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
   } else if (KIND == PASS_MID) {
     scw[SC_AP + A.j] += tot[0];
   } else {
-    const double nrm2 = tot[1];
-    const double beta = sqrt(nrm2);
-    scw[SC_AL + A.j] = alpha;
-    scw[SC_BE + A.j] = beta;
-    scw[SC_SG + A.j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
-    scw[SC_Q + A.j + 1] = nrm2 > 0.0 ? tot[2] / nrm2 : 0.0;
+    lanczos_scalars(scw, A.j, A.raw, alpha, tot[1], tot[2]);
   }
 }
 
@@ -870,12 +876,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
   } else if (KIND == PASS_MID) {
     scw[SC_AP + A.j] += tot[0];
   } else {
-    const double nrm2 = tot[1];
-    const double beta = sqrt(nrm2);
-    scw[SC_AL + A.j] = alpha;
-    scw[SC_BE + A.j] = beta;
-    scw[SC_SG + A.j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
-    scw[SC_Q + A.j + 1] = nrm2 > 0.0 ? tot[2] / nrm2 : 0.0;
+    lanczos_scalars(scw, A.j, A.raw, alpha, tot[1], tot[2]);
   }
 }
 
@@ -1333,17 +1334,21 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
   if (tid == 0) {
     *A.counter = 0u;
     A.sc[SC_N0SQ] = tot[0];
-    A.sc[SC_SG + 0] = tot[0] > 0.0 ? 1.0 / sqrt(tot[0]) : 0.0;
-    A.sc[SC_Q + 0] = tot[0] > 0.0 ? tot[1] / tot[0] : 0.0;
+    if (A.raw) {   // sharded: the host all-reduces ||psi||^2, <psi|A|psi> and the masks, then finishes
+      A.sc[SC_Q + 0] = tot[1];
+    } else {
+      A.sc[SC_SG + 0] = tot[0] > 0.0 ? 1.0 / sqrt(tot[0]) : 0.0;
+      A.sc[SC_Q + 0] = tot[0] > 0.0 ? tot[1] / tot[0] : 0.0;
+    }
   }
 }
 
 // ---------------------------------------------------------------- tables and helpers
 __global__ void build_dl_kernel(int a, int n, const double* __restrict__ umat, DiagArgs dg, int with_interaction,
-                                double* __restrict__ dl) {
+                                double offset, double* __restrict__ dl) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (1 << a)) return;
-  double v = 0.0;
+  double v = offset;   // sharded runs: the constant energy of the shard's global bits
   for (int i = 0; i < a; ++i) {
     if (!((e >> i) & 1)) continue;
     v -= dg.delta[i];
@@ -1464,6 +1469,26 @@ __global__ void lanczos_update_kernel(cplx* __restrict__ w, const cplx* __restri
     nn = fma(a.x, a.x, fma(a.y, a.y, nn));
   }
   double mine[1] = {block_sum<kThreads>(nn, red)};
+  double tot[1];
+  if (!grid_finalize<1, kThreads>(mine, part, counter, tot, red)) return;
+  if (threadIdx.x == 0) result[0] = tot[0];
+}
+
+// Flip of a sharded (global) qubit: u += c * x_peer (the partner shard's amplitudes, same local
+// index) and dot = Re <x|x_peer> for the qubit's share of alpha (sharding.py; krylov.py:96-99).
+__global__ void global_flip_kernel(cplx* __restrict__ u, const cplx* __restrict__ xp, const cplx* __restrict__ x,
+                                   double c, uint64_t n, double* part, unsigned* counter, double* result) {
+  __shared__ double red[32];
+  double dot = 0.0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const cplx p = xp[i], xi = x[i];
+    cplx a = u[i];
+    a.x = fma(c, p.x, a.x);
+    a.y = fma(c, p.y, a.y);
+    u[i] = a;
+    dot = fma(xi.x, p.x, fma(xi.y, p.y, dot));
+  }
+  double mine[1] = {block_sum<kThreads>(dot, red)};
   double tot[1];
   if (!grid_finalize<1, kThreads>(mine, part, counter, tot, red)) return;
   if (threadIdx.x == 0) result[0] = tot[0];
@@ -1632,13 +1657,13 @@ cudaError_t launch_chunk(const ChunkArgs& args, cudaStream_t st) {
 }
 
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
-                            double* dl, cudaStream_t st) {
+                            double offset, double* dl, cudaStream_t st) {
   DiagArgs dg{};
   if (delta_host != nullptr)
     for (int i = 0; i < n && i < kMaxQubits; ++i) dg.delta[i] = delta_host[i];
   const int total = 1 << a;
   const int nt = total < 256 ? total : 256;
-  build_dl_kernel<<<(total + nt - 1) / nt, nt, 0, st>>>(a, n, umat, dg, with_interaction, dl);
+  build_dl_kernel<<<(total + nt - 1) / nt, nt, 0, st>>>(a, n, umat, dg, with_interaction, offset, dl);
   return cudaGetLastError();
 }
 
@@ -1690,6 +1715,12 @@ cudaError_t launch_diff_norm(const cplx* x, const cplx* y, uint64_t n, double* p
 cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, double alpha, double beta, uint64_t n,
                                   double* part, unsigned* counter, double* result, int grid, cudaStream_t st) {
   lanczos_update_kernel<<<flat_grid(n, grid), kThreads, 0, st>>>(w, v, vprev, alpha, beta, n, part, counter, result);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_global_flip(cplx* u, const cplx* xp, const cplx* x, double c, uint64_t n, double* part,
+                               unsigned* counter, double* result, cudaStream_t st) {
+  global_flip_kernel<<<flat_grid(n, 0), kThreads, 0, st>>>(u, xp, x, c, n, part, counter, result);
   return cudaGetLastError();
 }
 

@@ -59,6 +59,7 @@ constexpr int SC_AL = SC_Q + 128; // alpha_j
 constexpr int SC_BE = SC_AL + 128;// beta_j
 constexpr int SC_SG = SC_BE + 128;// sigma_j : v_j = sigma_j * s_j
 constexpr int SC_OBS = SC_SG + 128;
+constexpr int SC_GF = SC_OBS + kMaxMasks;   // global-flip dot (sharded runs)
 constexpr int SC_SIZE = SC_OBS + kMaxMasks + 8;
 
 enum PassKind : int {
@@ -117,6 +118,7 @@ struct alignas(64) PassArgs {
   cplx* out;
   int j;                                // Lanczos iteration
   int qsweep;                           // LAST_LANCZOS: compute q_{j+1}
+  int raw;                              // LAST_LANCZOS of a sharded run: store local sums (host all-reduces)
   double* sc; double* part; unsigned* counter;
 };
 
@@ -131,6 +133,7 @@ struct CombineArgs {
   int qsweep;
   int nmask;                            // observables: sum_b |psi_b|^2 [b & M == M]
   uint64_t mask[kMaxMasks];
+  int raw;                              // sharded run: store local sums (host all-reduces)
   double* sc; double* part; unsigned* counter;
 };
 
@@ -166,7 +169,9 @@ cudaError_t launch_pass(const PassArgs& args, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st);
 cudaError_t launch_chunk(const ChunkArgs& args, cudaStream_t st);
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
-                            double* dl, cudaStream_t st);
+                            double offset, double* dl, cudaStream_t st);
+cudaError_t launch_global_flip(cplx* u, const cplx* xp, const cplx* x, double c, uint64_t n, double* part,
+                               unsigned* counter, double* result, cudaStream_t st);
 cudaError_t launch_tile_table(int a, int n, const double* umat, double* gc, cudaStream_t st);
 cudaError_t launch_tile_base(int a, int n, int fly, const double* delta_host, double* gc, cudaStream_t st);
 cudaError_t launch_interaction_diag(int n, const double* umat, const double* delta_host, double* dvec,

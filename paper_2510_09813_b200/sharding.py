@@ -321,3 +321,154 @@ def evolve_sv_sharded(seq, reg, dist, tolerance=1e-10, max_krylov_dim=100, initi
         iters.append(it)
     occ = sharded_occupations(plan, ops, comm, psi)
     return psi, iters, occ
+
+
+class FusedShardEngine:
+    """One shard of a sharded exact evolution on the fused Lanczos driver (rsv_expm_step).
+
+    The local qubits run the same bit-group pass kernels as a single GPU (effective detunings and
+    the shard's constant energy folded into the diagonal tables); the driver calls back into this
+    object for the collectives (include/rsv.h, rsv_comm_fn): all-reduces of the Lanczos scalars
+    (alpha partial, ||w||^2, <w|A_last|w>, ||psi||^2, observables) and, per global qubit with a
+    nonzero drive, the exchange of s_j with the partner shard -- the first one started before the
+    local passes so that it overlaps them (NCCL on its own stream); its flip and share of alpha
+    are applied by the global_flip kernel before the last pass.
+    """
+
+    def __init__(self, n_qubits: int, u, dist, *, device=None, max_krylov_dim: int = 100,
+                 memory_budget_bytes=None, krylov_vectors_cap=None):
+        import torch
+
+        from . import _native as nat
+        from .engine import SvEngine
+
+        self.torch = torch
+        self.nat = nat
+        self.dist = dist
+        self.plan = ShardPlan(n_qubits, dist.get_world_size(), dist.get_rank())
+        self.u = np.asarray(u, dtype=float)
+        nl = self.plan.n_local
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        # the exchange buffer first: the Krylov workspace takes what is left
+        self.xbuf = torch.empty(1 << nl, dtype=torch.complex128, device=dev)
+        self.eng = SvEngine(nl, self.u[:nl, :nl], diag="fly", max_krylov_dim=max_krylov_dim, device=dev,
+                            memory_budget_bytes=memory_budget_bytes, krylov_vectors_cap=krylov_vectors_cap)
+        self.nccl = dist.get_backend() == "nccl"
+        self._reqs = []
+        self._recv_host = None
+        self._cb = nat.COMM_FN(self._comm)   # keep the ctypes thunk alive
+        nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self._cb, None, self.xbuf.data_ptr()), "rsv_set_shard")
+        self.eng.set_observables([1 << q for q in range(nl)])
+        psi = self.eng.state()
+        psi.zero_()
+        if self.plan.rank == 0:
+            psi[0] = 1.0   # |0...0>: every global bit 0 lives on rank 0
+        nat.check(self.eng.lib.rsv_state_modified(self.eng.ctx))
+
+    # -- collectives requested by the C driver --------------------------------------
+    def _comm(self, _user, op, slot, peer, host, count):
+        try:
+            torch, dist, nat = self.torch, self.dist, self.nat
+            if op == nat.RSV_COMM_ALLREDUCE:
+                arr = np.ctypeslib.as_array(host, shape=(count,))
+                t = torch.from_numpy(arr.copy())
+                if self.nccl:
+                    t = t.to(self.device)
+                dist.all_reduce(t)
+                arr[:] = t.cpu().numpy()
+            elif op == nat.RSV_COMM_EXCHANGE_START:
+                send = self.eng.slots[slot]
+                if self.nccl:   # NCCL P2P on its own stream: overlaps the local passes
+                    ops = [dist.P2POp(dist.isend, send, peer), dist.P2POp(dist.irecv, self.xbuf, peer)]
+                else:           # gloo moves host tensors (CPU tests / one-GPU test boxes)
+                    self._send_host = send.cpu()
+                    self._recv_host = torch.empty_like(self._send_host)
+                    ops = [dist.P2POp(dist.isend, self._send_host, peer),
+                           dist.P2POp(dist.irecv, self._recv_host, peer)]
+                self._reqs = dist.batch_isend_irecv(ops)
+            elif op == nat.RSV_COMM_EXCHANGE_WAIT:
+                for r in self._reqs:
+                    r.wait()
+                self._reqs = []
+                if not self.nccl:
+                    self.xbuf.copy_(self._recv_host)
+                torch.cuda.current_stream(self.device).synchronize()
+            else:
+                return 2
+            return 0
+        except Exception:   # pragma: no cover - reported through the C error path
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    # -- one exact step ------------------------------------------------------------
+    def _local(self, omegas, deltas):
+        om_l, de_eff, _u, offset, _flips = self.plan.local_parameters(omegas, deltas, self.u)
+        coef = np.array([0.5 * float(omegas[g]) for g in self.plan.global_qubits], dtype=np.float64)
+        peer = np.array([self.plan.partner(g) for g in self.plan.global_qubits], dtype=np.int32)
+        return om_l, de_eff, offset, coef, peer
+
+    def step(self, omegas, deltas, dt_ns, tolerance=1e-10, max_krylov_dim=100, next_params=None,
+             observe=False, norm_epsilon=1e-14):
+        import ctypes
+
+        nat = self.nat
+        om_l, de_eff, offset, coef, peer = self._local(omegas, deltas)
+        nxt = None
+        next_offset = offset
+        if next_params is not None:
+            n_om, n_de, next_offset, _c, _p = self._local(*next_params)
+            nxt = (n_om, n_de)
+        self.eng.sync_stream()
+        nat.check(self.eng.lib.rsv_set_shard_step(
+            self.eng.ctx, float(offset), float(next_offset), len(coef), nat.dptr(coef),
+            peer.ctypes.data_as(ctypes.POINTER(ctypes.c_int))), "rsv_set_shard_step")
+        return self.eng.step(om_l, de_eff, dt_ns, tolerance, max_krylov_dim, norm_epsilon, next_params=nxt,
+                             observe=observe)
+
+    def occupations(self):
+        """<n_q> for all N qubits after an observed step: local qubits from the all-reduced mask sums,
+        global qubits from the shards' norms (rank bits)."""
+        import ctypes
+
+        occ_local = self.eng.observables()
+        loc = ctypes.c_double()
+        self.nat.check(self.eng.lib.rsv_shard_local_norm_sq(self.eng.ctx, ctypes.byref(loc)))
+        vals = [self.plan.global_bit(g) * loc.value for g in self.plan.global_qubits] + [loc.value]
+        tot = TorchComm(self.dist, self.device if self.nccl else None).allreduce_real(vals)
+        return np.concatenate([occ_local, tot[:-1] / tot[-1]])
+
+    def state(self):
+        return self.eng.state()
+
+    def close(self):
+        self.nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self.nat.COMM_FN(), None, None))
+        self.eng.close()
+
+
+def evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, max_krylov_dim=100, device=None,
+                            krylov_vectors_cap=None):
+    """Sharded exact evolution on the fused kernels (row e): returns (local final state, per-step
+    Krylov reports, occupations of all N qubits after the last step)."""
+    from .errors import SolverError
+    from .hamiltonian import interaction_matrix
+
+    eng = FusedShardEngine(reg.qubit_count, interaction_matrix(reg), dist, device=device,
+                           max_krylov_dim=max_krylov_dim, krylov_vectors_cap=krylov_vectors_cap)
+    reps = []
+    for k in range(seq.step_count):
+        nxt = seq.step(k + 1) if k + 1 < seq.step_count else None
+        rep = eng.step(*seq.step(k), float(seq.dt_ns), tolerance, max_krylov_dim, next_params=nxt,
+                       observe=(k + 1 == seq.step_count))
+        if not rep.converged:
+            raise SolverError(f"Krylov did not converge at step {k} (residual {rep.residual:.3e})", step=k,
+                              residual=rep.residual)
+        reps.append(rep)
+    occ = eng.occupations()
+    psi = eng.state().clone()
+    eng.close()
+    return psi, reps, occ
