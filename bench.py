@@ -11,8 +11,9 @@ step's occupations). Default: W=3 warm-up steps then K=97 timed steps = the whol
 value = H.psi products per second (whole job); ms_per_step; s_per_us_pulse; effective HBM
 GB/s (32 B per amplitude per H.psi: read psi, write H psi); roofline of the dominant kernel;
 e2e through the public API (evolve_sv) with host initial/final state; CPU baseline (C port of
-the reference's numba matvec, OpenMP on the host cores, bounded sample). Multi-GPU (torchrun):
-independent replicas per GPU (round 1: sharding by top qubits not yet wired), max over ranks.
+the reference's numba matvec, OpenMP on the host cores, bounded sample). Multi-GPU (torchrun, P GPUs):
+one register of N = n + log2(P) qubits sharded by its top qubits (weak scaling; run_sharded), max
+over ranks; --replicas runs P independent single-GPU copies instead.
 """
 
 from __future__ import annotations
@@ -167,13 +168,17 @@ def dist_setup(gpus):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if torch.cuda.is_available():
+        # one GPU per rank; modulo only so the sharded path can be smoke-tested with several ranks on
+        # a one-GPU box (RSV_BENCH_BACKEND=gloo)
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
     pg = None
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        backend = os.environ.get("RSV_BENCH_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
         pg = dist
     return rank, world, local, pg
 
@@ -256,10 +261,128 @@ def alg_bytes_per_launch(family, n, k_avg, diag):
     return (k_avg + 1) * 16 * amp
 
 
+def run_sharded(args, rank, world, local, pg):
+    """--gpus P > 1: one shard per GPU (row e), weak scaling: N = n + log2(P) qubits, 2^n amplitudes
+    per GPU. Local bit-group passes + global-qubit exchanges (NCCL P2P, the first overlapped with the
+    local passes) + all-reduced Lanczos scalars. value counts N=n-equivalent products (x 2^(N-n)), so
+    perfect weak scaling gives P x the one-GPU value."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_09813_b200 import KrylovConfig, interaction_matrix, workloads
+    from paper_2510_09813_b200.sharding import FusedShardEngine, evolve_sv_sharded_fused
+
+    n_glob = int(math.log2(world))
+    n_tot = args.n + n_glob
+    reg, seq = workloads.config(args.workload, dt_ns=args.dt, n_override=n_tot)
+    total_steps = args.warmup + args.steps
+    cfg = KrylovConfig(args.tol)
+    u = interaction_matrix(reg)
+    t_setup = time.time()
+    eng = FusedShardEngine(n_tot, u, dist, device=torch.device("cuda", local), max_krylov_dim=cfg.max_krylov_dim)
+    stream = torch.cuda.current_stream()
+
+    def do_step(k):
+        nxt = seq.step(k + 1) if k + 1 < seq.step_count else None
+        return eng.step(*seq.step(k), float(seq.dt_ns), cfg.tolerance, cfg.max_krylov_dim, next_params=nxt,
+                        observe=True)
+
+    for k in range(args.warmup):
+        do_step(k)
+    torch.cuda.synchronize()
+    barrier(pg)
+    eng.eng.set_profiling(True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    reps = [do_step(k) for k in range(args.warmup, total_steps)]
+    occ = eng.occupations()   # host read of the step's result (all-reduced)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier(pg)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), pg)
+    prof = eng.eng.profile()
+    matvecs = sum(r.matvecs for r in reps)
+    iters = [r.iterations for r in reps]
+    secs = ms / 1e3
+    scale = 2 ** (n_tot - args.n)
+    value = matvecs * scale / secs
+    fam = max(prof, key=lambda f: prof[f]["ms"])
+    k_avg = float(np.mean(iters)) if iters else 1.0
+    avg_launch_ms = prof[fam]["ms"] / max(1, prof[fam]["launches"])
+    alg = alg_bytes_per_launch(fam, args.n, k_avg, "fly")
+    achieved = alg / (avg_launch_ms / 1e3) / 1e9
+    hbm_peak, peak_kind = peaks()
+    krylov_cap = eng.eng.krylov_cap
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+
+    e2e = None
+    if not args.no_e2e:   # public API, host shard in (pinned) and out
+        host_in = torch.zeros(2 ** args.n, dtype=torch.complex128, pin_memory=True)
+        if rank == 0:
+            host_in[0] = 1.0
+        host_out = torch.empty(2 ** args.n, dtype=torch.complex128, pin_memory=True)
+        sub = type(seq)(seq.dt_ns, seq.omegas[:total_steps], seq.deltas[:total_steps], seq.dt_ns * total_steps)
+        torch.cuda.synchronize()
+        barrier(pg)
+        t0 = time.perf_counter()
+        psi, reps2, _occ = evolve_sv_sharded_fused(sub, reg, dist, tolerance=cfg.tolerance,
+                                                   device=torch.device("cuda", local), initial_local=host_in)
+        host_out.copy_(psi)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t0), pg)
+        mv2 = sum(r.matvecs for r in reps2)
+        e2e = {"value": mv2 * scale / (e2e_ms / 1e3), "unit": "H.psi/s",
+               "h2d_bytes_per_step": int(16 * 2 ** args.n / total_steps),
+               "d2h_bytes_per_step": int((16 * 2 ** args.n + 8 * n_tot * total_steps) / total_steps),
+               "steps": total_steps, "ms": e2e_ms,
+               "path": "paper_2510_09813_b200.sharding.evolve_sv_sharded_fused(host shard in) + shard copied out"}
+        del psi
+        torch.cuda.empty_cache()
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": value, "unit": "H.psi/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
+            "config": {
+                "workload": f"random{n_tot}: N={n_tot} random 2D register sharded by the top {n_glob} qubits "
+                            f"over {world} GPUs (2^{args.n} amplitudes per GPU), per-atom detuning map, "
+                            f"1 us pulse, dt={args.dt} ns, Krylov tol {args.tol}",
+                "n_qubits": n_tot, "n_local": args.n, "dt_ns": args.dt, "pulse_steps": seq.step_count,
+                "timed_steps": f"{args.warmup + 1}..{total_steps}", "diag": "fly",
+                "parallelism": f"{world} shards (top-qubit sharding, {dist.get_backend()} P2P exchange + all-reduce)",
+                "value_units": f"N={args.n}-equivalent H.psi: products x 2^(N - {args.n})",
+                "l2": "inputs larger than L2 (shard = %.1f GB)" % (16 * 2 ** args.n / 1e9),
+                "krylov_vectors_resident": krylov_cap,
+            },
+            "s_per_us_pulse": ms / args.steps * seq.step_count / 1e3 * (1000.0 / (seq.dt_ns * seq.step_count)),
+            "krylov": {"iterations_mean": k_avg, "iterations_max": max(iters) if iters else 0,
+                       "matvecs": matvecs, "substeps": sum(r.substeps for r in reps)},
+            "kernel_ms": {f: round(v["ms"], 3) for f, v in prof.items()},
+            "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm_peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "alg_bytes_per_launch": alg, "avg_launch_ms": avg_launch_ms},
+            "gpu_launches": int(sum(v["launches"] for v in prof.values())),
+            "clocks": clocks, "e2e": e2e, "cpu_baseline": None,
+            "final_occupations": [round(float(x), 6) for x in occ],
+            "setup_s": round(time.time() - t_setup, 1),
+        }
+        print(json.dumps(line), flush=True)
+    barrier(pg)
+    return 0
+
+
 def run_ours(args):
     import torch
 
     rank, world, local, pg = dist_setup(args.gpus)
+    if world > 1 and not args.replicas:
+        return run_sharded(args, rank, world, local, pg)
     from paper_2510_09813_b200 import KrylovConfig, ObservableSpec, SvRunConfig, evolve_sv, interaction_matrix
     from paper_2510_09813_b200 import workloads
     from paper_2510_09813_b200.engine import SvEngine
@@ -430,13 +553,15 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=97)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=29)
+    ap.add_argument("--qubits", "--n", dest="n", type=int, default=29)
     ap.add_argument("--workload", default="random29")
     ap.add_argument("--dt", type=int, default=10)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--diag", default="fly", choices=["fly", "vec"])
     ap.add_argument("--plan-gm", type=int, default=-1,
                     help="pass plan: -1 auto, 0 plain bit-group passes, 3..9 L2 chunk pass (A/B runs)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent N=--n replicas instead of one sharded N + log2(P) register")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

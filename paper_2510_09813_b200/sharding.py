@@ -336,7 +336,7 @@ class FusedShardEngine:
     """
 
     def __init__(self, n_qubits: int, u, dist, *, device=None, max_krylov_dim: int = 100,
-                 memory_budget_bytes=None, krylov_vectors_cap=None):
+                 memory_budget_bytes=None, krylov_vectors_cap=None, initial_local=None):
         import torch
 
         from . import _native as nat
@@ -363,9 +363,14 @@ class FusedShardEngine:
         nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self._cb, None, self.xbuf.data_ptr()), "rsv_set_shard")
         self.eng.set_observables([1 << q for q in range(nl)])
         psi = self.eng.state()
-        psi.zero_()
-        if self.plan.rank == 0:
-            psi[0] = 1.0   # |0...0>: every global bit 0 lives on rank 0
+        if initial_local is not None:   # this shard's amplitudes (host or device tensor)
+            if tuple(initial_local.shape) != (1 << nl,):
+                raise ValidationError(f"initial shard has shape {tuple(initial_local.shape)}, expected ({1 << nl},)")
+            psi.copy_(initial_local, non_blocking=True)
+        else:
+            psi.zero_()
+            if self.plan.rank == 0:
+                psi[0] = 1.0   # |0...0>: every global bit 0 lives on rank 0
         nat.check(self.eng.lib.rsv_state_modified(self.eng.ctx))
 
     # -- collectives requested by the C driver --------------------------------------
@@ -451,14 +456,16 @@ class FusedShardEngine:
 
 
 def evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, max_krylov_dim=100, device=None,
-                            krylov_vectors_cap=None):
+                            krylov_vectors_cap=None, initial_local=None):
     """Sharded exact evolution on the fused kernels (row e): returns (local final state, per-step
-    Krylov reports, occupations of all N qubits after the last step)."""
+    Krylov reports, occupations of all N qubits after the last step). ``initial_local``: this rank's
+    2^(N - log2 P) amplitudes (default |0...0>)."""
     from .errors import SolverError
     from .hamiltonian import interaction_matrix
 
     eng = FusedShardEngine(reg.qubit_count, interaction_matrix(reg), dist, device=device,
-                           max_krylov_dim=max_krylov_dim, krylov_vectors_cap=krylov_vectors_cap)
+                           max_krylov_dim=max_krylov_dim, krylov_vectors_cap=krylov_vectors_cap,
+                           initial_local=initial_local)
     reps = []
     for k in range(seq.step_count):
         nxt = seq.step(k + 1) if k + 1 < seq.step_count else None
