@@ -400,7 +400,8 @@ class FusedShardEngine:
                 self._reqs = []
                 if not self.nccl:
                     self.xbuf.copy_(self._recv_host)
-                torch.cuda.current_stream(self.device).synchronize()
+                if self.xbuf.is_cuda:
+                    torch.cuda.current_stream(self.device).synchronize()
             else:
                 return 2
             return 0

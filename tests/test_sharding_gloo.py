@@ -124,3 +124,51 @@ def test_plan_validation():
         ShardPlan(2, 4, 0)
     p = ShardPlan(33, 8, 5)
     assert p.n_local == 30 and p.global_qubits == [30, 31, 32] and p.partner(31) == 7
+
+
+def _comm_worker(rank, world, port, outdir):
+    """FusedShardEngine's collective callback (the function the C driver calls through rsv_comm_fn),
+    driven directly on host tensors over gloo: all-reduce in place, pairwise exchange into the buffer."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_09813_b200 import _native as nat
+    from paper_2510_09813_b200.sharding import FusedShardEngine
+
+    eng = FusedShardEngine.__new__(FusedShardEngine)   # no GPU: only the callback is exercised
+    eng.torch, eng.nat, eng.dist, eng.nccl = torch, nat, dist, False
+    eng.device = torch.device("cpu")
+    eng._reqs, eng._recv_host = [], None
+
+    class _Slots:
+        slots = [torch.full((8,), complex(rank, -rank), dtype=torch.complex128), torch.zeros(8, dtype=torch.complex128)]
+
+    eng.eng = _Slots()
+    eng.xbuf = torch.zeros(8, dtype=torch.complex128)
+    vals = (ctypes.c_double * 3)(1.0 + rank, 10.0 * rank, -1.0)
+    ok = [eng._comm(None, nat.RSV_COMM_ALLREDUCE, -1, -1, vals, 3)]
+    peer = rank ^ 1
+    ok.append(eng._comm(None, nat.RSV_COMM_EXCHANGE_START, 0, peer, None, 0))
+    ok.append(eng._comm(None, nat.RSV_COMM_EXCHANGE_WAIT, 0, peer, None, 0))
+    ok.append(eng._comm(None, 99, 0, 0, None, 0))
+    np.save(os.path.join(outdir, f"c{rank}.npy"), {"ok": ok, "vals": list(vals), "x": eng.xbuf.numpy()},
+            allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fused_shard_comm_callback(tmp_path):
+    import torch.multiprocessing as mp
+
+    world = 2
+    mp.spawn(_comm_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        d = np.load(tmp_path / f"c{r}.npy", allow_pickle=True).item()
+        assert d["ok"][:3] == [0, 0, 0] and d["ok"][3] != 0   # unknown op is reported, not ignored
+        assert d["vals"] == [3.0, 10.0, -2.0]
+        assert np.array_equal(d["x"], np.full(8, complex(r ^ 1, -(r ^ 1))))
