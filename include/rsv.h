@@ -101,6 +101,12 @@ int rsv_measure(rsv_context* ctx, double* out_host, double* norm_sq);
 int rsv_observe(rsv_context* ctx, const void* psi, const uint64_t* masks, int nmask, double* out_host,
                 double* norm_sq);
 /* sum_b |x_b - y_b|^2 (observables.py:137 norm_difference, computed without cancellation). */
+/* Basis-state indices drawn from |psi|^2 by inverse CDF (replaces observables.py:167 sample_bitstrings,
+ * dense path): `uniforms` are the reference's per-batch PCG64 draws (host), out_indices[s] = the first
+ * index whose cumulative |psi|^2 exceeds uniforms[s] * ||psi||^2 (searchsorted side="right"; cdf[-1] = 1).
+ * norm_sq (may be NULL) returns ||psi||^2 for the caller's normalisation check. psi has 2^n amplitudes. */
+int rsv_sample(rsv_context* ctx, const void* psi, const double* uniforms, int64_t shots, int64_t* out_indices,
+               double* norm_sq);
 int rsv_diff_norm_sq(rsv_context* ctx, const void* x, const void* y, uint64_t n, double* out);
 
 /* Generic vector kernels for the callable-matvec Lanczos (krylov.py:96-121). */

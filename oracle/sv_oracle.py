@@ -209,6 +209,24 @@ def norm_difference(a, b):
 
 # ---------------------------------------------------------------- time stepping
 
+def sample_bitstrings(psi, shots, seed):
+    """Dense inverse-CDF sampling with the reference's batched PCG64 streams (observables.py:167-214)."""
+    probs = np.abs(np.asarray(psi)) ** 2
+    probs = probs / probs.sum()
+    cdf = np.cumsum(probs)
+    cdf[-1] = 1.0
+    batch = 4096   # observables.py:34
+    counts = [min(batch, shots - s) for s in range(0, shots, batch)]
+    streams = np.random.SeedSequence(seed).spawn(len(counts))
+    out = np.empty(shots, dtype=np.int64)
+    pos = 0
+    for count, stream in zip(counts, streams):
+        rng = np.random.Generator(np.random.PCG64(stream))
+        out[pos:pos + count] = np.searchsorted(cdf, rng.random(count), side="right")
+        pos += count
+    return out
+
+
 def memory_estimate_sv(n_qubits, krylov_dim):
     """16 * 2^N * (k + 2) bytes (sv.py:45)."""
     if n_qubits < 1 or krylov_dim < 0:

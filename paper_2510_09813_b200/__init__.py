@@ -33,6 +33,7 @@ from .observables import (  # noqa: F401
     occupation,
     occupations,
     overlap,
+    sample_bitstrings,
 )
 from .pulses import (  # noqa: F401
     Blackman,

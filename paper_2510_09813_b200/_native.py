@@ -74,6 +74,8 @@ SIGNATURES = {
     "rsv_measure": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p]),
     "rsv_observe": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, c_u64_p, ctypes.c_int, c_double_p,
                                    c_double_p]),
+    "rsv_sample": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, c_double_p, ctypes.c_int64,
+                                  ctypes.POINTER(ctypes.c_int64), c_double_p]),
     "rsv_diff_norm_sq": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                         c_double_p]),
     "rsv_zdotc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, c_double_p]),

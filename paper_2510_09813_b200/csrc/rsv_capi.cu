@@ -1171,6 +1171,44 @@ int rsv_observe(rsv_context* c, const void* psi, const uint64_t* masks, int nmas
   return RSV_OK;
 }
 
+int rsv_sample(rsv_context* c, const void* psi, const double* uniforms, int64_t shots, int64_t* out_indices,
+               double* norm_sq) {
+  if (!c || !psi || !uniforms || !out_indices) return fail(RSV_ERR_ARG, "NULL argument");
+  if (shots < 1) return fail(RSV_ERR_ARG, "shots must be >= 1, got %lld", (long long)shots);
+  const uint64_t n = 1ull << c->n;
+  const uint64_t chunks = (n + 4095) / 4096;
+  double* d_sums = nullptr;
+  double* d_u = nullptr;
+  int64_t* d_out = nullptr;
+  int rc = RSV_OK;
+  cudaError_t e = cudaMallocAsync(&d_sums, sizeof(double) * (chunks + 1), c->st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_u, sizeof(double) * shots, c->st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_out, sizeof(int64_t) * shots, c->st);
+  uint64_t nchunks = 0;
+  std::vector<double> pre(chunks + 1, 0.0);
+  if (e == cudaSuccess) e = rsv::launch_chunk_norms(reinterpret_cast<const cplx*>(psi), n, d_sums, &nchunks, c->st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pre.data() + 1, d_sums, sizeof(double) * nchunks, cudaMemcpyDeviceToHost, c->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (e == cudaSuccess) {
+    for (uint64_t i = 1; i <= nchunks; ++i) pre[i] += pre[i - 1];   // exclusive chunk prefix, in order
+    if (norm_sq) *norm_sq = pre[nchunks];
+    e = cudaMemcpyAsync(d_sums, pre.data(), sizeof(double) * (nchunks + 1), cudaMemcpyHostToDevice, c->st);
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, uniforms, sizeof(double) * shots, cudaMemcpyHostToDevice, c->st);
+  if (e == cudaSuccess)
+    e = rsv::launch_sample(reinterpret_cast<const cplx*>(psi), n, d_sums, nchunks, d_u, pre[nchunks], shots, d_out,
+                           c->st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out_indices, d_out, sizeof(int64_t) * shots, cudaMemcpyDeviceToHost, c->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) rc = fail(RSV_ERR_CUDA, "rsv_sample: %s", cudaGetErrorString(e));
+  cudaFreeAsync(d_sums, c->st);
+  cudaFreeAsync(d_u, c->st);
+  cudaFreeAsync(d_out, c->st);
+  return rc;
+}
+
 int rsv_diff_norm_sq(rsv_context* c, const void* x, const void* y, uint64_t n, double* out) {
   if (!c) return fail(RSV_ERR_ARG, "NULL context");
   CUDA_TRY(rsv::launch_diff_norm(reinterpret_cast<const cplx*>(x), reinterpret_cast<const cplx*>(y), n, c->d_part,

@@ -1494,6 +1494,71 @@ __global__ void global_flip_kernel(cplx* __restrict__ u, const cplx* __restrict_
   if (threadIdx.x == 0) result[0] = tot[0];
 }
 
+// ---- bitstring sampling (observables.py:167 sample_bitstrings, dense inverse-CDF path)
+// chunk sums of |psi|^2 in a fixed order; the host prefixes them (float64) and each shot is
+// resolved by one warp: binary search over the chunk prefixes, then a warp-scan walk inside
+// the chunk to the first index whose running sum exceeds u * total (searchsorted side="right").
+constexpr int kSampleChunkLog2 = 12;
+
+__global__ void chunk_norms_kernel(const cplx* __restrict__ psi, uint64_t n, double* __restrict__ sums) {
+  __shared__ double red[32];
+  const uint64_t chunk = 1ull << kSampleChunkLog2;
+  const uint64_t base = (uint64_t)blockIdx.x * chunk;
+  const uint64_t len = n - base < chunk ? n - base : chunk;
+  double v = 0.0;
+  for (uint64_t i = threadIdx.x; i < len; i += kThreads) {
+    const cplx a = psi[base + i];
+    v = fma(a.x, a.x, fma(a.y, a.y, v));
+  }
+  v = block_sum<kThreads>(v, red);
+  if (threadIdx.x == 0) sums[blockIdx.x] = v;
+}
+
+__global__ void sample_kernel(const cplx* __restrict__ psi, uint64_t n, const double* __restrict__ prefix,
+                              uint64_t nchunks, const double* __restrict__ u, double total, int64_t shots,
+                              int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t shot = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (shot >= shots) return;
+  const double target = u[shot] * total;
+  // largest chunk c with prefix[c] <= target (prefix[0] = 0, prefix[nchunks] = total)
+  uint64_t lo = 0, hi = nchunks;   // invariant: prefix[lo] <= target, answer < hi
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= target) lo = mid;
+    else hi = mid;
+  }
+  const uint64_t chunk = 1ull << kSampleChunkLog2;
+  int64_t result = (int64_t)n - 1;   // cdf[-1] = 1: a target at or past the total maps to the last index
+  for (uint64_t c = lo; c < nchunks; ++c) {
+    double running = prefix[c];
+    const uint64_t base = c * chunk;
+    const uint64_t len = n - base < chunk ? n - base : chunk;
+    bool found = false;
+    for (uint64_t off = 0; off < len; off += 32) {
+      double v = 0.0;
+      if (off + lane < len) {
+        const cplx a = psi[base + off + lane];
+        v = fma(a.x, a.x, a.y * a.y);
+      }
+      #pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {   // inclusive warp scan (fixed order)
+        const double t = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += t;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, (off + lane < len) && (running + v > target));
+      if (hit) {
+        result = (int64_t)(base + off + (uint64_t)(__ffs(hit) - 1));
+        found = true;
+        break;
+      }
+      running += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (found) break;
+  }
+  if (lane == 0) out[shot] = result;
+}
+
 __global__ void axpy_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, double2 a, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const cplx b = x[i];
@@ -1721,6 +1786,21 @@ cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, dou
 cudaError_t launch_global_flip(cplx* u, const cplx* xp, const cplx* x, double c, uint64_t n, double* part,
                                unsigned* counter, double* result, cudaStream_t st) {
   global_flip_kernel<<<flat_grid(n, 0), kThreads, 0, st>>>(u, xp, x, c, n, part, counter, result);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_norms(const cplx* psi, uint64_t n, double* sums, uint64_t* nchunks, cudaStream_t st) {
+  const uint64_t chunk = 1ull << kSampleChunkLog2;
+  *nchunks = (n + chunk - 1) / chunk;
+  chunk_norms_kernel<<<(unsigned)*nchunks, kThreads, 0, st>>>(psi, n, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample(const cplx* psi, uint64_t n, const double* prefix, uint64_t nchunks, const double* u,
+                          double total, int64_t shots, int64_t* out, cudaStream_t st) {
+  const int warps = kThreads / 32;
+  const uint64_t blocks = (uint64_t)(shots + warps - 1) / warps;
+  sample_kernel<<<(unsigned)blocks, kThreads, 0, st>>>(psi, n, prefix, nchunks, u, total, shots, out);
   return cudaGetLastError();
 }
 

@@ -184,6 +184,9 @@ cudaError_t launch_lanczos_update(cplx* w, const cplx* v, const cplx* vprev, dou
                                   uint64_t n, double* part, unsigned* counter, double* result, int grid,
                                   cudaStream_t st);
 cudaError_t launch_axpy(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
+cudaError_t launch_chunk_norms(const cplx* psi, uint64_t n, double* sums, uint64_t* nchunks, cudaStream_t st);
+cudaError_t launch_sample(const cplx* psi, uint64_t n, const double* prefix, uint64_t nchunks, const double* u,
+                          double total, int64_t shots, int64_t* out, cudaStream_t st);
 cudaError_t launch_scale(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
 int max_grid_rows();   // upper bound on the grid of any kernel writing partial rows
 

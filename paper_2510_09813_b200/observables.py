@@ -1,7 +1,7 @@
 """Measurements on device-resident states -- mirror of rydsim/observables.py (dense-state part).
 
 ``occupations`` (observables.py:82), ``occupation`` (:95), ``correlation`` (:102),
-``overlap`` (:120), ``norm_difference`` (:137), ``fidelity`` (:157),
+``overlap`` (:120), ``norm_difference`` (:137), ``fidelity`` (:157), ``sample_bitstrings`` (:167),
 ``ObservableSpec`` (:221) and ``ObservableRecord`` (:263) with the reference's
 names and validation. The reductions run in the rsv kernels: an observable is a
 bit mask M with value sum_b |psi_b|^2 [b & M == M] / sum_b |psi_b|^2.
@@ -35,7 +35,45 @@ __all__ = [
     "qubit_count",
     "format_bitstring",
     "occupation_masks",
+    "sample_bitstrings",
 ]
+
+_SAMPLE_BATCH = 4096       # observables.py:34
+_NORM_TOLERANCE = 1e-6     # observables.py:35
+
+
+def sample_uniforms(shots: int, seed: int) -> np.ndarray:
+    """The reference's uniform draws (observables.py:194-213): one PCG64 child stream of
+    SeedSequence(seed) per batch of 4096 shots, so the samples do not depend on the execution."""
+    batches = [min(_SAMPLE_BATCH, shots - start) for start in range(0, shots, _SAMPLE_BATCH)]
+    streams = np.random.SeedSequence(seed).spawn(len(batches))
+    out = np.empty(shots, dtype=np.float64)
+    pos = 0
+    for count, stream in zip(batches, streams):
+        out[pos:pos + count] = np.random.Generator(np.random.PCG64(stream)).random(count)
+        pos += count
+    return out
+
+
+def sample_bitstrings(state, shots: int, seed: int, renormalize: bool = False) -> np.ndarray:
+    """Basis-state indices drawn from |amplitude|^2 (observables.py:167, dense path), on the device:
+    the state never leaves HBM (inverse CDF: chunk sums -> prefix -> one warp per shot)."""
+    if shots < 1:
+        raise ValidationError(f"shots must be >= 1, got {shots}")
+    n = qubit_count(state)
+    x = _dev(state)
+    u = sample_uniforms(int(shots), int(seed))
+    out = np.empty(int(shots), dtype=np.int64)
+    nsq = ctypes.c_double()
+    ctx = _ctx(n)
+    nat.check(ctx.lib.rsv_sample(ctx.ctx, x.data_ptr(), nat.dptr(u), int(shots),
+                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(nsq)),
+              "rsv_sample")
+    norm = math.sqrt(max(0.0, nsq.value))
+    if abs(norm - 1.0) > _NORM_TOLERANCE and not renormalize:
+        raise ValidationError(f"state norm deviates from 1 by {abs(norm - 1.0):.3e}; "
+                              "pass renormalize=True to sample anyway")
+    return out
 
 
 def qubit_count(state) -> int:

@@ -228,7 +228,29 @@ def gen_diag_checks():
     np.savez_compressed(os.path.join(HERE, "diagonal.npz"), **out)
 
 
+def gen_sampling():
+    """rydsim.observables.sample_bitstrings on random normalised states (dense inverse-CDF path)."""
+    from rydsim.observables import sample_bitstrings
+
+    out = {}
+    for n, shots, seed in ((1, 50, 1), (5, 1000, 7), (10, 5000, 2025), (14, 9000, 3)):
+        rng = np.random.default_rng(400 + n)
+        psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        if n == 10:   # a peaked state: most of the weight on a few indices
+            psi[rng.integers(0, 2 ** n, 3)] *= 40.0
+        psi /= np.linalg.norm(psi)
+        out[f"n{n}_psi"] = psi
+        out[f"n{n}_shots"] = shots
+        out[f"n{n}_seed"] = seed
+        out[f"n{n}_idx"] = sample_bitstrings(psi, shots, seed)
+    np.savez_compressed(os.path.join(HERE, "sampling.npz"), **out)
+
+
 if __name__ == "__main__":
+    if "--sampling" in sys.argv:   # regenerate only the sampling fixture
+        gen_sampling()
+        sys.exit(0)
+    gen_sampling()
     gen_apply()
     gen_expm()
     gen_diag_checks()

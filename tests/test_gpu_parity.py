@@ -281,3 +281,46 @@ class TestFullSize:
         back = eng.step(om, de, -10.0, 1e-10, 100)
         assert back.converged
         assert rs.norm_difference(eng.state(), psi0) <= 1e-8
+
+
+class TestSampling:
+    """Device inverse-CDF sampling (observables.py:167) against the reference's own draws."""
+
+    def test_golden_indices(self, rs, torch):
+        g = load("sampling.npz")
+        for n in (1, 5, 10, 14):
+            psi = torch.from_numpy(g[f"n{n}_psi"]).cuda()
+            idx = rs.sample_bitstrings(psi, int(g[f"n{n}_shots"]), int(g[f"n{n}_seed"]))
+            assert np.array_equal(idx, g[f"n{n}_idx"]), n
+
+    def test_against_oracle_and_edges(self, rs, torch):
+        rng = np.random.default_rng(12)
+        for n in (12, 13, 17):   # one chunk, two chunks, many chunks
+            psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+            psi[: 2 ** n // 3] = 0.0    # leading zero-probability run
+            psi /= np.linalg.norm(psi)
+            idx = rs.sample_bitstrings(torch.from_numpy(psi).cuda(), 20000, 99)
+            assert np.array_equal(idx, O.sample_bitstrings(psi, 20000, 99)), n
+            assert idx.min() >= 2 ** n // 3
+        basis = np.zeros(2 ** 15, complex)
+        basis[2 ** 15 - 1] = 1.0        # all weight on the last index
+        assert np.all(rs.sample_bitstrings(basis, 100, 1) == 2 ** 15 - 1)
+        with pytest.raises(rs.ValidationError):
+            rs.sample_bitstrings(2 * basis, 10, 1)
+        assert np.all(rs.sample_bitstrings(2 * basis, 10, 1, renormalize=True) == 2 ** 15 - 1)
+        with pytest.raises(rs.ValidationError):
+            rs.sample_bitstrings(basis, 0, 1)
+
+    def test_full_size_histogram(self, rs, torch):
+        # N=27 (2^27 amplitudes, 2 GB): per-qubit frequencies of 2^16 shots match the occupations
+        n = 27
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        psi = torch.randn(2 ** n, dtype=torch.complex128, device="cuda", generator=gen)
+        psi *= torch.exp(-torch.arange(2 ** n, device="cuda", dtype=torch.float64) / 2 ** 25)
+        psi /= torch.linalg.vector_norm(psi)
+        shots = 1 << 16
+        idx = rs.sample_bitstrings(psi, shots, 17)
+        occ = rs.occupations(psi)
+        freq = np.array([((idx >> q) & 1).mean() for q in range(n)])
+        sigma = np.sqrt(occ * (1 - occ) / shots) + 1e-12
+        assert np.all(np.abs(freq - occ) <= 6 * sigma)

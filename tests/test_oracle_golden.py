@@ -128,3 +128,22 @@ class TestPulsesOracle:
         assert O.discretize(x, 1)[:, 0].tolist() == [0.5, 1.5, 2.5, 3.0]
         assert O.memory_estimate_sv(1, 1) == 96
         assert O.memory_estimate_sv(26, 15) < 20e9
+
+
+class TestSamplingOracle:
+    def test_sampling_matches_reference(self):
+        g = load("sampling.npz")
+        for n in (1, 5, 10, 14):
+            idx = O.sample_bitstrings(g[f"n{n}_psi"], int(g[f"n{n}_shots"]), int(g[f"n{n}_seed"]))
+            assert np.array_equal(idx, g[f"n{n}_idx"]), n
+
+    def test_reference_uniform_streams(self):
+        # the host half of the device sampler draws exactly the reference's uniforms
+        from paper_2510_09813_b200.observables import sample_uniforms
+
+        g = load("sampling.npz")
+        psi = g["n10_psi"]
+        cdf = np.cumsum(np.abs(psi) ** 2 / np.sum(np.abs(psi) ** 2))
+        cdf[-1] = 1.0
+        u = sample_uniforms(int(g["n10_shots"]), int(g["n10_seed"]))
+        assert np.array_equal(np.searchsorted(cdf, u, side="right"), g["n10_idx"])
