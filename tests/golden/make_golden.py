@@ -246,10 +246,60 @@ def gen_sampling():
     np.savez_compressed(os.path.join(HERE, "sampling.npz"), **out)
 
 
+def _segment_doc(seg):
+    d = {"kind": type(seg).__name__, "duration_ns": seg.duration_ns}
+    for k in ("value", "start", "stop", "area", "points"):
+        if hasattr(seg, k):
+            v = getattr(seg, k)
+            d[k] = [list(p) for p in v] if k == "points" else v
+    return d
+
+
+def gen_runs():
+    """rydsim.runner.execute_run (backend sv) on the reference's own sequence/config fixtures and on a
+    variant with correlations, snapshots, an initial bitstring and samples. The inputs are stored as a
+    plain program description (register + segments) that the tests rebuild with the mirror's types."""
+    from rydsim.observables import ObservableSpec as RefSpec
+    from rydsim.runner import execute_run
+    from rydsim.sequence_io import parse_config, parse_sequence
+
+    cfg_dir = "/root/reference/pkg/configs"
+    reg, prog = parse_sequence(os.path.join(cfg_dir, "sequence_adiabatic_5q.json"))
+    base = parse_config(os.path.join(cfg_dir, "run_sv.json"))
+    import dataclasses
+
+    variants = {
+        "adiabatic5": base,
+        "adiabatic5_var": dataclasses.replace(
+            base, dt_ns=20, initial_bits=0b00100, seed=11, sample_shots=3000, snapshot_every=10,
+            observables=(RefSpec("occupation", (0, 2, 4), 5), RefSpec("correlation", (0, 1, 1, 3), 0))),
+    }
+    out = {}
+    for name, cfg in variants.items():
+        doc = execute_run(reg, prog, cfg).strip_volatile()
+        out[name] = {"document": doc,
+                     "register": {"positions_um": [list(p) for p in reg.positions_um],
+                                  "interaction_c": reg.interaction_c},
+                     "program": {"duration_ns": prog.duration_ns,
+                                 "omega": [[_segment_doc(s) for s in ch] for ch in prog.omega],
+                                 "delta": [[_segment_doc(s) for s in ch] for ch in prog.delta]},
+                     "config": {"dt_ns": cfg.dt_ns, "initial_bits": cfg.initial_bits, "seed": cfg.seed,
+                                "sample_shots": cfg.sample_shots, "snapshot_every": cfg.snapshot_every,
+                                "tolerance": cfg.krylov.tolerance, "max_krylov_dim": cfg.krylov.max_krylov_dim,
+                                "observables": [[s.kind, list(s.qubits), s.every_n_steps]
+                                                for s in cfg.observables]}}
+    with open(os.path.join(HERE, "runs_sv.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 if __name__ == "__main__":
     if "--sampling" in sys.argv:   # regenerate only the sampling fixture
         gen_sampling()
         sys.exit(0)
+    if "--runs" in sys.argv:       # regenerate only the run-document fixture
+        gen_runs()
+        sys.exit(0)
+    gen_runs()
     gen_sampling()
     gen_apply()
     gen_expm()

@@ -246,7 +246,8 @@ class TestFullSize:
     """BASELINE configs[3] size (N=29) through size-independent properties."""
 
     @pytest.fixture(scope="class")
-    def setup29(self, rs, torch):
+    @staticmethod
+    def setup29(rs, torch):
         from paper_2510_09813_b200 import workloads
         from paper_2510_09813_b200.engine import SvEngine
 
