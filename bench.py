@@ -279,7 +279,9 @@ def run_sharded(args, rank, world, local, pg):
     cfg = KrylovConfig(args.tol)
     u = interaction_matrix(reg)
     t_setup = time.time()
-    eng = FusedShardEngine(n_tot, u, dist, device=torch.device("cuda", local), max_krylov_dim=cfg.max_krylov_dim)
+    eng = FusedShardEngine(n_tot, u, dist, device=torch.device("cuda", local), max_krylov_dim=cfg.max_krylov_dim,
+                           peer_memory=not args.no_peer_memory)
+    peer_mode = eng.peer_memory
     stream = torch.cuda.current_stream()
 
     def do_step(k):
@@ -332,7 +334,8 @@ def run_sharded(args, rank, world, local, pg):
         barrier(pg)
         t0 = time.perf_counter()
         psi, reps2, _occ = evolve_sv_sharded_fused(sub, reg, dist, tolerance=cfg.tolerance,
-                                                   device=torch.device("cuda", local), initial_local=host_in)
+                                                   device=torch.device("cuda", local), initial_local=host_in,
+                                                   peer_memory=not args.no_peer_memory)
         host_out.copy_(psi)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t0), pg)
@@ -355,7 +358,9 @@ def run_sharded(args, rank, world, local, pg):
                             f"1 us pulse, dt={args.dt} ns, Krylov tol {args.tol}",
                 "n_qubits": n_tot, "n_local": args.n, "dt_ns": args.dt, "pulse_steps": seq.step_count,
                 "timed_steps": f"{args.warmup + 1}..{total_steps}", "diag": "fly",
-                "parallelism": f"{world} shards (top-qubit sharding, {dist.get_backend()} P2P exchange + all-reduce)",
+                "parallelism": (f"{world} shards (top-qubit sharding; global-qubit flips by "
+                                + ("P2P loads of the partner shards (CUDA IPC peer mappings)" if peer_mode
+                                   else f"{dist.get_backend()} exchange") + f"; {dist.get_backend()} all-reduce)"),
                 "value_units": f"N={args.n}-equivalent H.psi: products x 2^(N - {args.n})",
                 "l2": "inputs larger than L2 (shard = %.1f GB)" % (16 * 2 ** args.n / 1e9),
                 "krylov_vectors_resident": krylov_cap,
@@ -560,6 +565,8 @@ def main(argv=None):
     ap.add_argument("--diag", default="fly", choices=["fly", "vec"])
     ap.add_argument("--plan-gm", type=int, default=-1,
                     help="pass plan: -1 auto, 0 plain bit-group passes, 3..9 L2 chunk pass (A/B runs)")
+    ap.add_argument("--no-peer-memory", action="store_true",
+                    help="N > 1: exchange the partner shards' vectors instead of reading them over NVLink")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent N=--n replicas instead of one sharded N + log2(P) register")
     ap.add_argument("--no-e2e", action="store_true")

@@ -136,6 +136,11 @@ int rsv_set_shard(rsv_context* ctx, rsv_comm_fn comm, void* user, void* exchange
  * Omega_g/2 (0 = no flip) with the partner rank. */
 int rsv_set_shard_step(rsv_context* ctx, double offset, double next_offset, int n_global, const double* coef,
                        const int* peer);
+/* Peer-memory mode: ptrs[g * nslots + s] = bound slot s of the partner shard of global qubit g, mapped
+ * into this process (CUDA IPC over NVLink / UVA). The first pass then reads the partner shards' s_j
+ * directly (P2P loads) instead of exchanging copies; n_global = 0 returns to the exchange mode.
+ * Plans with a single pass keep the exchange. */
+int rsv_set_shard_peers(rsv_context* ctx, int n_global, const void* const* ptrs, int nslots);
 /* This shard's share of ||psi||^2 from the last Krylov combination / measurement. */
 int rsv_shard_local_norm_sq(rsv_context* ctx, double* out);
 

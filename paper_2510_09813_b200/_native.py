@@ -91,6 +91,8 @@ SIGNATURES = {
     "rsv_set_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                           c_double_p, c_int_p]),
     "rsv_shard_local_norm_sq": (ctypes.c_int, [ctypes.c_void_p, c_double_p]),
+    "rsv_set_shard_peers": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                           ctypes.c_int]),
     "rsv_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_get_profile": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_ll_p]),
     "rsv_reset_profile": (ctypes.c_int, [ctypes.c_void_p]),

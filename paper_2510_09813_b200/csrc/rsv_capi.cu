@@ -226,6 +226,9 @@ struct rsv_context {
   std::vector<int> gpeer;           // partner rank of each global qubit
   double n0sq_global = 0.0;         // ||psi||^2 over all shards from the last combination
   double local_n0sq = 0.0;          // this shard's share of it
+  // peer-memory mode: the partner shards' slots mapped into this process (CUDA IPC / UVA);
+  // peer_slots[g][physical slot] for global qubit g (empty: exchange through the callback)
+  std::vector<std::vector<const cplx*>> peer_slots;
   int plan_gm = -1;               // chunk group bits: -1 auto, 0 off, 3..9 forced (rsv_set_plan)
   long long plan_lag = -1;        // chunk scheduler lag in M tiles (-1 auto)
   unsigned long long* d_ticket = nullptr;
@@ -521,11 +524,11 @@ int shard_finish_combine(rsv_context* c, int nmask) {
 // Before the last pass of iteration j: the global-qubit flips (partner shard's s_j, exchanged by the
 // host) are added to the partial sums u (slot j+1), and alpha's partial share is all-reduced.
 // The first exchange was started before the local passes (overlapped with them).
-int shard_before_last(rsv_context* c, int j, double sigma, bool started) {
+int shard_before_last(rsv_context* c, int j, double sigma, bool started, bool p2p) {
   double add = 0.0;
   const uint64_t nloc = 1ull << c->n;
   bool first = true;
-  for (size_t g = 0; g < c->gcoef.size(); ++g) {
+  for (size_t g = 0; g < c->gcoef.size() && !p2p; ++g) {
     if (c->gcoef[g] == 0.0) continue;
     int rc;
     if (!(first && started)) {
@@ -677,8 +680,10 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
                              double prev_coef) {
   const size_t np = c->plan.size();
   // sharded: start the first global-qubit exchange of s_j so it overlaps the local passes
+  // (peer-memory mode: no exchange, the first pass reads the partner shards directly)
   bool started = false;
-  if (c->sharded) {
+  const bool p2p = c->sharded && !c->peer_slots.empty() && np > 1;
+  if (c->sharded && !p2p) {
     for (size_t g = 0; g < c->gcoef.size(); ++g) {
       if (c->gcoef[g] == 0.0) continue;
       CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -701,7 +706,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
           CUDA_TRY(cudaMemsetAsync(slot(c, j + 1), 0, sizeof(cplx) * nloc, c->st));
         }
       }
-      int rc = shard_before_last(c, j, sigma, started);
+      int rc = shard_before_last(c, j, sigma, started, p2p);
       if (rc) return rc;
     }
     if (p.chunk) {
@@ -735,6 +740,14 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
       A.ein_is_prev = 0;
     }
     A.out = slot(c, j + 1);   // u in place, then s_{j+1}
+    if (p2p && pi == 0) {
+      for (size_t g = 0; g < c->gcoef.size(); ++g) {
+        if (c->gcoef[g] == 0.0) continue;
+        A.peer[A.npeer] = c->peer_slots[g][c->logical[j]];
+        A.peer_coef[A.npeer] = c->gcoef[g];
+        ++A.npeer;
+      }
+    }
     A.qsweep = last ? 1 : 0;
     A.raw = (last && c->sharded) ? 1 : 0;
     set_tile_load(A);
@@ -1296,6 +1309,25 @@ int rsv_set_shard_step(rsv_context* c, double offset, double next_offset, int n_
   c->next_offset = next_offset;
   c->gcoef.assign(coef, coef + n_global);
   c->gpeer.assign(peer, peer + n_global);
+  return RSV_OK;
+}
+
+int rsv_set_shard_peers(rsv_context* c, int n_global, const void* const* ptrs, int nslots) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (n_global == 0 || ptrs == nullptr) {
+    c->peer_slots.clear();
+    return RSV_OK;
+  }
+  if (n_global < 0 || n_global > 4) return fail(RSV_ERR_ARG, "peer-memory mode supports 1..4 global qubits, got %d", n_global);
+  if (nslots != (int)c->phys.size()) return fail(RSV_ERR_ARG, "peer table has %d slots, %d are bound", nslots, (int)c->phys.size());
+  c->peer_slots.assign(n_global, std::vector<const cplx*>(nslots, nullptr));
+  for (int g = 0; g < n_global; ++g)
+    for (int s = 0; s < nslots; ++s) {
+      const void* p = ptrs[(size_t)g * nslots + s];
+      if (p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u))
+        return fail(RSV_ERR_ARG, "peer slot (%d, %d) is NULL or misaligned", g, s);
+      c->peer_slots[g][s] = reinterpret_cast<const cplx*>(p);
+    }
   return RSV_OK;
 }
 

@@ -581,6 +581,21 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
         ac[i].y = fma(d, xv[i].y, ac[i].y);
       }
     }
+    // sharded runs in peer-memory mode: the flips on the global qubits read the partner shards'
+    // x (same local index) straight from their HBM over NVLink; they are part of this pass's
+    // operator, so they also enter <x|A x> (alpha's partial share)
+    for (int g = 0; g < A.npeer; ++g) {
+      const cplx* pp = A.peer[g] + g0;
+      const double c = A.peer_coef[g] * xs;
+      cplx pv[EPT];
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) pv[i] = __ldcg(pp + i * S);
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        ac[i].x = fma(c, pv[i].x, ac[i].x);
+        ac[i].y = fma(c, pv[i].y, ac[i].y);
+      }
+    }
     if (has_e) {
       mbar_wait(&bars[2], ephase);
       ephase ^= 1u;

@@ -119,6 +119,9 @@ struct alignas(64) PassArgs {
   int j;                                // Lanczos iteration
   int qsweep;                           // LAST_LANCZOS: compute q_{j+1}
   int raw;                              // LAST_LANCZOS of a sharded run: store local sums (host all-reduces)
+  int npeer;                            // sharded, peer-memory mode (first pass): global-qubit flips
+  const cplx* peer[4];                  //   read the partner shards' x over NVLink (P2P loads)
+  double peer_coef[4];                  //   Omega_g / 2
   double* sc; double* part; unsigned* counter;
 };
 

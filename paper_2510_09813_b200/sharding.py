@@ -336,7 +336,7 @@ class FusedShardEngine:
     """
 
     def __init__(self, n_qubits: int, u, dist, *, device=None, max_krylov_dim: int = 100,
-                 memory_budget_bytes=None, krylov_vectors_cap=None, initial_local=None):
+                 memory_budget_bytes=None, krylov_vectors_cap=None, initial_local=None, peer_memory=False):
         import torch
 
         from . import _native as nat
@@ -362,6 +362,10 @@ class FusedShardEngine:
         self._cb = nat.COMM_FN(self._comm)   # keep the ctypes thunk alive
         nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self._cb, None, self.xbuf.data_ptr()), "rsv_set_shard")
         self.eng.set_observables([1 << q for q in range(nl)])
+        self.peer_memory = False
+        self._peer_tensors = []
+        if peer_memory:
+            self.peer_memory = self._map_peers()
         psi = self.eng.state()
         if initial_local is not None:   # this shard's amplitudes (host or device tensor)
             if tuple(initial_local.shape) != (1 << nl,):
@@ -372,6 +376,38 @@ class FusedShardEngine:
             if self.plan.rank == 0:
                 psi[0] = 1.0   # |0...0>: every global bit 0 lives on rank 0
         nat.check(self.eng.lib.rsv_state_modified(self.eng.ctx))
+
+    def _map_peers(self) -> bool:
+        """Peer-memory mode: map every partner shard's Krylov slots into this process (CUDA IPC;
+        on an NVLink box the mapping is a peer mapping, so the first pass reads them with P2P
+        loads). All ranks agree on the outcome; on any failure they stay in exchange mode."""
+        import ctypes
+
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        torch, dist, nat = self.torch, self.dist, self.nat
+        ok = 1.0
+        try:
+            mine = [reduce_tensor(t) for t in self.eng.slots]
+            everyone = [None] * dist.get_world_size()
+            dist.all_gather_object(everyone, mine)
+            table = []
+            for g in self.plan.global_qubits:
+                peer = self.plan.partner(g)
+                tensors = [fn(*args) for fn, args in everyone[peer]]
+                self._peer_tensors.append(tensors)
+                table.extend(t.data_ptr() for t in tensors)
+        except Exception:   # pragma: no cover - platform without CUDA IPC
+            ok = 0.0
+        flag = torch.tensor([ok], dtype=torch.float64, device=self.device if self.nccl else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if flag.item() < 1.0:
+            self._peer_tensors = []
+            return False
+        ng, ns = len(self.plan.global_qubits), len(self.eng.slots)
+        arr = (ctypes.c_void_p * (ng * ns))(*table)
+        nat.check(self.eng.lib.rsv_set_shard_peers(self.eng.ctx, ng, arr, ns), "rsv_set_shard_peers")
+        return True
 
     # -- collectives requested by the C driver --------------------------------------
     def _comm(self, _user, op, slot, peer, host, count):
@@ -452,21 +488,28 @@ class FusedShardEngine:
         return self.eng.state()
 
     def close(self):
+        self.nat.check(self.eng.lib.rsv_set_shard_peers(self.eng.ctx, 0, None, 0))
         self.nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self.nat.COMM_FN(), None, None))
+        self.dist.barrier()   # partners may still read this shard's slots until everyone is done
+        self._peer_tensors = []
         self.eng.close()
 
 
 def evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, max_krylov_dim=100, device=None,
-                            krylov_vectors_cap=None, initial_local=None):
+                            krylov_vectors_cap=None, initial_local=None, peer_memory=False, info=None):
     """Sharded exact evolution on the fused kernels (row e): returns (local final state, per-step
     Krylov reports, occupations of all N qubits after the last step). ``initial_local``: this rank's
-    2^(N - log2 P) amplitudes (default |0...0>)."""
+    2^(N - log2 P) amplitudes (default |0...0>). ``peer_memory``: read the partner shards through
+    CUDA IPC mappings instead of exchanging copies (falls back to the exchange if unavailable;
+    ``info["peer_memory"]`` tells which ran)."""
     from .errors import SolverError
     from .hamiltonian import interaction_matrix
 
     eng = FusedShardEngine(reg.qubit_count, interaction_matrix(reg), dist, device=device,
                            max_krylov_dim=max_krylov_dim, krylov_vectors_cap=krylov_vectors_cap,
-                           initial_local=initial_local)
+                           initial_local=initial_local, peer_memory=peer_memory)
+    if info is not None:   # which global-flip mode actually ran
+        info["peer_memory"] = eng.peer_memory
     reps = []
     for k in range(seq.step_count):
         nxt = seq.step(k + 1) if k + 1 < seq.step_count else None

@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, outdir, n, k0, steps, cap):
+def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False):
     import torch
     import torch.distributed as dist
 
@@ -37,7 +37,10 @@ def _worker(rank, world, port, outdir, n, k0, steps, cap):
     reg, full = workloads.config("random29", n_override=n)
     om, de = full.omegas[k0:k0 + steps], full.deltas[k0:k0 + steps]
     seq = rs.DiscretizedSequence(10, om, de, 10 * steps)
-    psi, reps, occ = evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, krylov_vectors_cap=cap)
+    info = {}
+    psi, reps, occ = evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, krylov_vectors_cap=cap,
+                                             peer_memory=peer, info=info)
+    assert info["peer_memory"] == peer   # the requested global-flip mode really ran
     np.save(os.path.join(outdir, f"s{rank}.npy"), psi.cpu().numpy())
     if rank == 0:
         np.save(os.path.join(outdir, "occ.npy"), occ)
@@ -49,14 +52,18 @@ def _worker(rank, world, port, outdir, n, k0, steps, cap):
 
 
 @pytest.mark.timeout(400)
-@pytest.mark.parametrize("world,n,cap", [(2, 14, None), (4, 14, None), (2, 17, None), (2, 14, 6)])
-def test_fused_sharded_evolution(tmp_path, world, n, cap):
+@pytest.mark.parametrize("world,n,cap,peer", [(2, 14, None, False), (4, 14, None, False), (2, 17, None, False),
+                                              (2, 14, 6, False), (2, 17, None, True), (4, 16, None, True),
+                                              (2, 15, 6, True)])
+def test_fused_sharded_evolution(tmp_path, world, n, cap, peer):
     # (4, 14): 12 local qubits -> one lo pass carries the diagonal, the shard offset and the q-sweep;
-    # (2, 17): 16 local qubits -> lo + one group pass; cap 6 forces exact sub-stepping across shards
+    # (2, 17): 16 local qubits -> lo + one group pass; cap 6 forces exact sub-stepping across shards;
+    # peer=True: peer-memory mode (the first pass reads the partner shards' slots through CUDA IPC --
+    # here on the same device, over NVLink on a multi-GPU box)
     import torch.multiprocessing as mp
 
     k0, steps = 30, 4
-    mp.spawn(_worker, args=(world, _port(), str(tmp_path), n, k0, steps, cap), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path), n, k0, steps, cap, peer), nprocs=world, join=True)
     psi = np.concatenate([np.load(tmp_path / f"s{r}.npy") for r in range(world)])
     inp = np.load(tmp_path / "in.npy", allow_pickle=True).item()
     from paper_2510_09813_b200.workloads import C6_RB70
