@@ -581,6 +581,36 @@ int shard_finish_iteration(rsv_context* c, int j) {
   return RSV_OK;
 }
 
+// Single-bit observable masks (occupations) are reduced per bit class in the combination kernel:
+// a bit of the combine tile is a thread-index bit (tile position < log2 threads) or a register bit,
+// any other bit is constant over a tile.
+void classify_masks(rsv::CombineArgs& A) {
+  A.obs_single = A.nmask > 0 ? 1 : 0;
+  const int lt = rsv::ilog2(rsv::combine_threads(A.sh.a + A.sh.g));
+  for (int m = 0; m < A.nmask; ++m) {
+    const uint64_t M = A.mask[m];
+    if (M == 0 || (M & (M - 1))) {
+      A.obs_single = 0;
+      return;
+    }
+    int q = 0;
+    while (!((M >> q) & 1ull)) ++q;
+    int pos = -1;   // tile position
+    if (q < A.sh.a) pos = q;
+    else if (q >= A.sh.p && q < A.sh.p + A.sh.g) pos = A.sh.a + (q - A.sh.p);
+    if (pos < 0) {
+      A.obs_cat[m] = 0;
+      A.obs_pos[m] = (unsigned char)q;
+    } else if (pos < lt) {
+      A.obs_cat[m] = 1;
+      A.obs_pos[m] = (unsigned char)pos;
+    } else {
+      A.obs_cat[m] = 2;
+      A.obs_pos[m] = (unsigned char)(pos - lt);
+    }
+  }
+}
+
 // Krylov combination (also "prepare": k = 1, coefficient 1, in place).
 int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, const double* q_omegas,
                 const double* q_deltas, int observe, double q_offset = 0.0) {
@@ -608,6 +638,7 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
   A.out = out;
   A.nmask = observe ? (int)c->masks.size() : 0;
   for (int m = 0; m < A.nmask; ++m) A.mask[m] = c->masks[m];
+  classify_masks(A);
   A.sc = c->d_sc;
   A.part = c->d_part;
   A.counter = c->d_counter;
@@ -1168,6 +1199,7 @@ int rsv_observe(rsv_context* c, const void* psi, const uint64_t* masks, int nmas
   A.qsweep = 0;
   A.nmask = nmask;
   for (int m = 0; m < nmask; ++m) A.mask[m] = masks[m];
+  classify_masks(A);
   A.sc = c->d_sc;
   A.part = c->d_part;
   A.counter = c->d_counter;

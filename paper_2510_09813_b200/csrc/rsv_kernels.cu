@@ -1208,6 +1208,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool has_diag = A.qsweep && A.dg.mode != DIAG_NONE;
   for (int m = lane; m < A.nmask; m += 32) s_obs[warp][m] = 0.0;
+  // single-bit masks (occupations): a bit is a register bit of the thread, a thread-index bit or
+  // constant over the tile; per-thread accumulators replace the per-mask warp reduction of every
+  // tile (one warp sum per tile for the tile-constant bits, block sums once at the end)
+  constexpr int LT = Log2<NT>::value;
+  const bool single = A.obs_single != 0;
+  double occ_p = 0.0, occ_r[RB > 0 ? RB : 1];
+  #pragma unroll
+  for (int b = 0; b < RB; ++b) occ_r[b] = 0.0;
   double acc_n = 0.0, acc_q = 0.0;
   uint64_t off[EPT];
   #pragma unroll
@@ -1297,7 +1305,22 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
       }
       __syncthreads();
     }
-    if (A.nmask > 0) {
+    if (A.nmask > 0 && single) {
+      double ps = 0.0;
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const double pi = wv[i].x * wv[i].x + wv[i].y * wv[i].y;
+        ps += pi;
+        #pragma unroll
+        for (int b = 0; b < RB; ++b)
+          if ((i >> b) & 1) occ_r[b] += pi;
+      }
+      occ_p += ps;
+      const double wsum = warp_sum<NT>(ps);
+      if (lane == 0)
+        for (int m = 0; m < A.nmask; ++m)
+          if (A.obs_cat[m] == 0 && ((g0 >> A.obs_pos[m]) & 1ull)) s_obs[warp][m] += wsum;
+    } else if (A.nmask > 0) {
       double p[EPT];
       #pragma unroll
       for (int i = 0; i < EPT; ++i) p[i] = wv[i].x * wv[i].x + wv[i].y * wv[i].y;
@@ -1321,10 +1344,27 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
     A.part[(size_t)blockIdx.x * stride + 0] = mine[0];
     A.part[(size_t)blockIdx.x * stride + 1] = mine[1];
   }
+  __shared__ double s_bit[16];   // single-bit masks: CTA sums per thread-index bit / register bit
+  if (single && A.nmask > 0) {
+    for (int pos = 0; pos < LT; ++pos) {
+      const double v = block_sum<NT>(((tid >> pos) & 1) ? occ_p : 0.0, red);
+      if (tid == 0) s_bit[pos] = v;
+    }
+    #pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const double v = block_sum<NT>(occ_r[b], red);
+      if (tid == 0) s_bit[LT + b] = v;
+    }
+    __syncthreads();
+  }
   for (int m = tid; m < A.nmask; m += NT) {
     double v = 0.0;
-    #pragma unroll
-    for (int w = 0; w < NW; ++w) v += s_obs[w][m];
+    if (single && A.obs_cat[m] != 0) {
+      v = s_bit[A.obs_cat[m] == 1 ? A.obs_pos[m] : LT + A.obs_pos[m]];
+    } else {
+      #pragma unroll
+      for (int w = 0; w < NW; ++w) v += s_obs[w][m];
+    }
     A.part[(size_t)blockIdx.x * stride + 2 + m] = v;
   }
   __shared__ bool s_last;

@@ -137,6 +137,9 @@ struct CombineArgs {
   int nmask;                            // observables: sum_b |psi_b|^2 [b & M == M]
   uint64_t mask[kMaxMasks];
   int raw;                              // sharded run: store local sums (host all-reduces)
+  int obs_single;                       // every mask is one bit: obs_cat 0 = constant over the tile
+  unsigned char obs_cat[kMaxMasks];     //   (obs_pos = global bit), 1 = thread-index bit, 2 = register
+  unsigned char obs_pos[kMaxMasks];     //   bit of the thread (obs_pos = that bit's index)
   double* sc; double* part; unsigned* counter;
 };
 
