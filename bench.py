@@ -273,7 +273,10 @@ def run_sharded(args, rank, world, local, pg):
     from paper_2510_09813_b200.sharding import FusedShardEngine, evolve_sv_sharded_fused
 
     n_glob = int(math.log2(world))
-    n_tot = args.n + n_glob
+    strong = args.total_qubits is not None   # BASELINE configs[4]: fixed N (e.g. 33) over P GPUs
+    n_tot = args.total_qubits if strong else args.n + n_glob
+    if strong:
+        args.n = n_tot - n_glob
     reg, seq = workloads.config(args.workload, dt_ns=args.dt, n_override=n_tot)
     total_steps = args.warmup + args.steps
     cfg = KrylovConfig(args.tol)
@@ -310,7 +313,7 @@ def run_sharded(args, rank, world, local, pg):
     matvecs = sum(r.matvecs for r in reps)
     iters = [r.iterations for r in reps]
     secs = ms / 1e3
-    scale = 2 ** (n_tot - args.n)
+    scale = 1 if strong else 2 ** (n_tot - args.n)
     value = matvecs * scale / secs
     fam = max(prof, key=lambda f: prof[f]["ms"])
     k_avg = float(np.mean(iters)) if iters else 1.0
@@ -350,7 +353,8 @@ def run_sharded(args, rank, world, local, pg):
     if rank == 0:
         line = {
             "metric": BASELINE_METRIC, "value": value, "unit": "H.psi/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
             "config": {
                 "workload": f"random{n_tot}: N={n_tot} random 2D register sharded by the top {n_glob} qubits "
@@ -361,7 +365,8 @@ def run_sharded(args, rank, world, local, pg):
                 "parallelism": (f"{world} shards (top-qubit sharding; global-qubit flips by "
                                 + ("P2P loads of the partner shards (CUDA IPC peer mappings)" if peer_mode
                                    else f"{dist.get_backend()} exchange") + f"; {dist.get_backend()} all-reduce)"),
-                "value_units": f"N={args.n}-equivalent H.psi: products x 2^(N - {args.n})",
+                "value_units": (f"H.psi of the N={n_tot} register" if strong
+                                else f"N={args.n}-equivalent H.psi: products x 2^(N - {args.n})"),
                 "l2": "inputs larger than L2 (shard = %.1f GB)" % (16 * 2 ** args.n / 1e9),
                 "krylov_vectors_resident": krylov_cap,
             },
@@ -565,6 +570,8 @@ def main(argv=None):
     ap.add_argument("--diag", default="fly", choices=["fly", "vec"])
     ap.add_argument("--plan-gm", type=int, default=-1,
                     help="pass plan: -1 auto, 0 plain bit-group passes, 3..9 L2 chunk pass (A/B runs)")
+    ap.add_argument("--total-qubits", type=int, default=None,
+                    help="N > 1: strong scaling of a fixed register (BASELINE configs[4]: 33) instead of n + log2 P")
     ap.add_argument("--no-peer-memory", action="store_true",
                     help="N > 1: exchange the partner shards' vectors instead of reading them over NVLink")
     ap.add_argument("--replicas", action="store_true",

@@ -131,7 +131,8 @@ int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass:
 #define RSV_COMM_EXCHANGE_START 2
 #define RSV_COMM_EXCHANGE_WAIT 3
 typedef int (*rsv_comm_fn)(void* user, int op, int slot, int peer, double* host, int count);
-int rsv_set_shard(rsv_context* ctx, rsv_comm_fn comm, void* user, void* exchange_buffer);
+int rsv_set_shard(rsv_context* ctx, rsv_comm_fn comm, void* user, void* exchange_buffer);   /* buffer may be NULL
+                                                     in peer-memory mode (rsv_set_shard_peers) */
 /* This step's constant energy of the shard's global bits (and the next step's), and per global qubit
  * Omega_g/2 (0 = no flip) with the partner rank. */
 int rsv_set_shard_step(rsv_context* ctx, double offset, double next_offset, int n_global, const double* coef,

@@ -530,6 +530,7 @@ int shard_before_last(rsv_context* c, int j, double sigma, bool started, bool p2
   bool first = true;
   for (size_t g = 0; g < c->gcoef.size() && !p2p; ++g) {
     if (c->gcoef[g] == 0.0) continue;
+    if (c->xbuf == nullptr) return fail(RSV_ERR_STATE, "exchange mode without an exchange buffer (rsv_set_shard)");
     int rc;
     if (!(first && started)) {
       CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -717,6 +718,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
   if (c->sharded && !p2p) {
     for (size_t g = 0; g < c->gcoef.size(); ++g) {
       if (c->gcoef[g] == 0.0) continue;
+      if (c->xbuf == nullptr) return fail(RSV_ERR_STATE, "exchange mode without an exchange buffer (rsv_set_shard)");
       CUDA_TRY(cudaStreamSynchronize(c->st));
       int rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[j], c->gpeer[g], nullptr, 0);
       if (rc) return rc;
@@ -1321,8 +1323,8 @@ int rsv_set_shard(rsv_context* c, rsv_comm_fn comm, void* user, void* exchange_b
     c->xbuf = nullptr;
     return RSV_OK;
   }
-  if (exchange_buffer == nullptr || (reinterpret_cast<uintptr_t>(exchange_buffer) & 15u))
-    return fail(RSV_ERR_ARG, "exchange buffer is NULL or not 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(exchange_buffer) & 15u)   // NULL: peer-memory mode only
+    return fail(RSV_ERR_ARG, "exchange buffer is not 16-byte aligned");
   c->sharded = true;
   c->comm = comm;
   c->comm_user = user;

@@ -337,6 +337,8 @@ class FusedShardEngine:
 
     def __init__(self, n_qubits: int, u, dist, *, device=None, max_krylov_dim: int = 100,
                  memory_budget_bytes=None, krylov_vectors_cap=None, initial_local=None, peer_memory=False):
+        import ctypes
+
         import torch
 
         from . import _native as nat
@@ -352,20 +354,31 @@ class FusedShardEngine:
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
-        # the exchange buffer first: the Krylov workspace takes what is left
-        self.xbuf = torch.empty(1 << nl, dtype=torch.complex128, device=dev)
         self.eng = SvEngine(nl, self.u[:nl, :nl], diag="fly", max_krylov_dim=max_krylov_dim, device=dev,
                             memory_budget_bytes=memory_budget_bytes, krylov_vectors_cap=krylov_vectors_cap)
         self.nccl = dist.get_backend() == "nccl"
         self._reqs = []
         self._recv_host = None
-        self._cb = nat.COMM_FN(self._comm)   # keep the ctypes thunk alive
-        nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self._cb, None, self.xbuf.data_ptr()), "rsv_set_shard")
-        self.eng.set_observables([1 << q for q in range(nl)])
         self.peer_memory = False
         self._peer_tensors = []
-        if peer_memory:
+        if peer_memory and len(self.eng.pass_plan()) > 1:   # single-pass plans keep the exchange
             self.peer_memory = self._map_peers()
+        # exchange mode needs a buffer for the partner's copy: a small one, or the last Krylov slot
+        # when the shard is large (all of HBM went to the slots)
+        self.xbuf = None
+        if not self.peer_memory:
+            if nl <= 20 or len(self.eng.slots) < 4:
+                self.xbuf = torch.empty(1 << nl, dtype=torch.complex128, device=dev)
+            else:
+                self.xbuf = self.eng.slots.pop()
+                ptrs = (ctypes.c_void_p * len(self.eng.slots))(*[t.data_ptr() for t in self.eng.slots])
+                nat.check(self.eng.lib.rsv_bind_slots(self.eng.ctx, ptrs, len(self.eng.slots)), "rsv_bind_slots")
+                self.eng.krylov_cap -= 1
+        self._cb = nat.COMM_FN(self._comm)   # keep the ctypes thunk alive
+        nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self._cb, None,
+                                             self.xbuf.data_ptr() if self.xbuf is not None else None),
+                  "rsv_set_shard")
+        self.eng.set_observables([1 << q for q in range(nl)])
         psi = self.eng.state()
         if initial_local is not None:   # this shard's amplitudes (host or device tensor)
             if tuple(initial_local.shape) != (1 << nl,):
