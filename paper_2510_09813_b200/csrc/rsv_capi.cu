@@ -714,7 +714,8 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
   // sharded: start the first global-qubit exchange of s_j so it overlaps the local passes
   // (peer-memory mode: no exchange, the first pass reads the partner shards directly)
   bool started = false;
-  const bool p2p = c->sharded && !c->peer_slots.empty() && np > 1;
+  // (the opt-in chunk pass has no peer operands: with it the exchange mode is required)
+  const bool p2p = c->sharded && !c->peer_slots.empty() && np > 1 && !c->plan[0].chunk;
   if (c->sharded && !p2p) {
     for (size_t g = 0; g < c->gcoef.size(); ++g) {
       if (c->gcoef[g] == 0.0) continue;

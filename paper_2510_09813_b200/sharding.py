@@ -361,7 +361,8 @@ class FusedShardEngine:
         self._recv_host = None
         self.peer_memory = False
         self._peer_tensors = []
-        if peer_memory and len(self.eng.pass_plan()) > 1:   # single-pass plans keep the exchange
+        plan = self.eng.pass_plan()
+        if peer_memory and len(plan) > 1 and plan[0]["family"] != "chunk":   # else the exchange is used
             self.peer_memory = self._map_peers()
         # exchange mode needs a buffer for the partner's copy: a small one, or the last Krylov slot
         # when the shard is large (all of HBM went to the slots)
