@@ -16,6 +16,10 @@
 #ifndef RSV_TMA
 #define RSV_TMA 1
 #endif
+// timing experiments only: skip the last pass's q-sweep (wrong Lanczos coefficients)
+#ifndef RSV_QSWEEP_OFF
+#define RSV_QSWEEP_OFF 0
+#endif
 // rotating tile buffers: the elementwise operand is prefetched one tile ahead too (pass_kernel_rot)
 #ifndef RSV_ROT
 #define RSV_ROT 1
@@ -836,7 +840,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
       st_stream(po + i * S, ac[i]);
     }
 
-    if (LANCZOS && A.qsweep) {
+    if (LANCZOS && A.qsweep && !RSV_QSWEEP_OFF) {
       // w goes to the operand buffer of this tile (refilled only after the next barrier A);
       // without an operand that buffer is idle
       cplx* sw = buf + be * TILE;
@@ -860,13 +864,16 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
         }
         acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
       }
+      // each pair (e, e^m) once: the partner with bit m clear takes the even amplitudes, the one
+      // with bit m set the odd ones -- every thread works on every flip (no idle half-warps/warps)
       for (int f = 0; f < A.fl.count; ++f) {
         const int m = A.fl.mask[f];
-        if (tid & m) continue;
+        const int own = (tid & m) ? 1 : 0;
         const cplx* ps = sw + (tid ^ m);
         const double c2 = 2.0 * A.fl.coef[f];
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
+          if ((i & 1) != own) continue;
           const cplx p = ps[i * NT];
           acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
         }
