@@ -40,6 +40,16 @@ except Exception:  # pragma: no cover
     BASELINE_METRIC = "H.psi/sec and effective HBM GB/s at N=29 (1 GPU)/N=33 (8 GPU); s per 1 us pulse"
 
 
+WORKLOAD_TEXT = {   # BASELINE.json configs
+    "random29": ("random 2D register (mean spacing 7 um, min 6 um, C6 = 2pi*862690), per-atom detuning map "
+                 "0.6..1, Blackman Omega peak 3pi rad/us, delta -6..6 rad/us, 1 us pulse (configs[3])"),
+    "lattice27": ("3x9 square lattice, 6.5 um spacing, global Blackman pulse Omega peak 3pi rad/us, delta -6..6 "
+                  "rad/us, 1 us (configs[2]: the paper's A100 40 GB limit)"),
+    "lattice20": "4x5 square lattice, 5.6 um spacing, adiabatic delta sweep -6..6 rad/us over 3 us (configs[1])",
+    "ring10": "ring register, constant Omega = 2pi rad/us, delta = 0, 1 us (configs[0])",
+}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -522,9 +532,8 @@ def run_ours(args):
             "dtype": "complex128 (f64)",
             "data": "synthetic",
             "config": {
-                "workload": f"{args.workload}: N={n} random 2D register (mean spacing 7 um, min 6 um, "
-                            "C6 = 2pi*862690), per-atom detuning map 0.6..1, Blackman Omega peak 3pi rad/us, "
-                            f"delta -6..6 rad/us, 1 us pulse, dt={args.dt} ns, Krylov tol {args.tol}",
+                "workload": f"{args.workload}: N={n} " + WORKLOAD_TEXT.get(args.workload, args.workload)
+                            + f", dt={args.dt} ns, Krylov tol {args.tol}",
                 "n_qubits": n, "dt_ns": args.dt, "pulse_steps": seq.step_count,
                 "timed_steps": f"{args.warmup + 1}..{total_steps}",
                 "diag": args.diag,
