@@ -3,6 +3,7 @@ exposes one GPU per call, so exchanges are staged through host memory; on an 8-G
 runs NCCL P2P) must reproduce the unsharded CPU oracle (reference sv.py:80 / krylov.py:67 restated in
 oracle/sv_oracle.py): fidelity 1 - |<ref|psi>|^2 <= 1e-10, occupations within 1e-8."""
 
+import math
 import os
 import socket
 
@@ -78,3 +79,73 @@ def test_fused_sharded_evolution(tmp_path, world, n, cap, peer):
         assert max(inp["sub"]) >= 1
     else:
         assert np.abs(np.array(inp["iters"]) - np.array(ref["iterations"])).max() <= 1
+
+
+def _probe_overlap(psi, start):
+    """<p|psi> for the deterministic probe p_b = exp(2 pi i frac(b * 0.6180339887...)) over global
+    indices start .. start + len(psi) - 1, in 2^24 chunks (never materialises the full probe)."""
+    import torch
+
+    tot = 0.0 + 0.0j
+    chunk = 1 << 24
+    for off in range(0, psi.numel(), chunk):
+        n = min(chunk, psi.numel() - off)
+        b = torch.arange(start + off, start + off + n, device=psi.device, dtype=torch.float64)
+        ph = 2 * math.pi * torch.frac(b * 0.6180339887498949)
+        p = torch.polar(torch.ones_like(ph), ph)
+        tot += complex(torch.sum(torch.conj(p) * psi[off:off + n]).item())
+    return tot
+
+
+def _full_worker(rank, world, port, outdir, n, k0, steps, cap):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2510_09813_b200 as rs
+    from paper_2510_09813_b200 import workloads
+    from paper_2510_09813_b200.sharding import evolve_sv_sharded_fused
+
+    reg, full = workloads.config("random29", n_override=n)
+    seq = rs.DiscretizedSequence(10, full.omegas[k0:k0 + steps], full.deltas[k0:k0 + steps], 10 * steps)
+    info = {}
+    psi, reps, occ = evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, krylov_vectors_cap=cap,
+                                             peer_memory=True, info=info)
+    ov = _probe_overlap(psi, rank * psi.numel())
+    nsq = float(torch.sum(torch.abs(psi) ** 2).item())
+    np.save(os.path.join(outdir, f"f{rank}.npy"), {"ov": ov, "nsq": nsq, "occ": occ, "peer": info["peer_memory"],
+                                                   "sub": sum(r.substeps for r in reps)}, allow_pickle=True)
+    del psi
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(900)
+def test_full_size_sharded_matches_single_gpu(tmp_path):
+    """N=28 (2 shards of 2^27 amplitudes, peer-memory mode, Krylov cap 10 so steps split) against the
+    single-GPU path at the same size, through size-independent properties: the overlap with a fixed
+    probe vector, the norm and all occupations."""
+    import torch
+    import torch.multiprocessing as mp
+
+    n, k0, steps, cap = 28, 40, 3, 10
+    mp.spawn(_full_worker, args=(2, _port(), str(tmp_path), n, k0, steps, cap), nprocs=2, join=True)
+    parts = [np.load(tmp_path / f"f{r}.npy", allow_pickle=True).item() for r in range(2)]
+    assert all(p["peer"] for p in parts) and sum(p["sub"] for p in parts) > 0
+    import paper_2510_09813_b200 as rs
+    from paper_2510_09813_b200 import workloads
+
+    reg, full = workloads.config("random29", n_override=n)
+    seq = rs.DiscretizedSequence(10, full.omegas[k0:k0 + steps], full.deltas[k0:k0 + steps], 10 * steps)
+    res = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-10), krylov_vectors_cap=cap,
+                                                observables=(rs.ObservableSpec("occupation", (), 0),)))
+    ov = _probe_overlap(res.final_state, 0)
+    assert abs(parts[0]["ov"] + parts[1]["ov"] - ov) <= 1e-9 * max(1.0, abs(ov))
+    assert abs(parts[0]["nsq"] + parts[1]["nsq"] - 1.0) <= 1e-9
+    occ = np.array(res.observables[-1].values)
+    assert np.abs(parts[0]["occ"] - occ).max() <= 1e-8
+    del res
+    torch.cuda.empty_cache()
