@@ -338,6 +338,9 @@ std::vector<PassPlan> hi_groups(int n, int from) {
 #ifndef RSV_CHUNK_DELEGATE
 #define RSV_CHUNK_DELEGATE 3
 #endif
+#ifndef RSV_CHUNK_DELEGATE_M
+#define RSV_CHUNK_DELEGATE_M 0
+#endif
 
 void build_plan(rsv_context* c) {
   const int n = c->n;
@@ -364,6 +367,11 @@ void build_plan(rsv_context* c) {
       PassPlan& m = c->plan[1];
       l.qubits.erase(l.qubits.begin(), l.qubits.begin() + d);
       for (int q = 0; q < d; ++q) m.qubits.push_back(q);
+    } else if (RSV_CHUNK_DELEGATE_M > 0 && lo.shm.a >= RSV_CHUNK_DELEGATE_M) {
+      // or to the chunk's own M tiles (they hold bits [0, 12 - gm) too)
+      PassPlan& l = c->plan[0];
+      l.qubits.erase(l.qubits.begin(), l.qubits.begin() + RSV_CHUNK_DELEGATE_M);
+      for (int q = 0; q < RSV_CHUNK_DELEGATE_M; ++q) l.qubits_m.push_back(q);
     }
     return;
   }
