@@ -761,7 +761,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     const bool last = pi + 1 == np;
     A.kind = last ? rsv::PASS_LAST_LANCZOS : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
-    A.fl = flips_for(p, omegas, rsv::pass_threads(p.sh.a + p.sh.g));
+    A.fl = flips_for(p, omegas, rsv::pass_threads_for(p.sh.a + p.sh.g, A.kind, p.sh.a));
     A.dg = diag_for(c, p, deltas);
     A.x = slot(c, j);
     A.x_scale_slot = rsv::SC_SG + j;
@@ -1114,7 +1114,7 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     rsv::PassArgs A{};
     A.kind = pi + 1 == np ? rsv::PASS_LAST_APPLY : (pi == 0 ? rsv::PASS_FIRST : rsv::PASS_MID);
     A.sh = p.sh;
-    A.fl = flips_for(p, omegas, rsv::pass_threads(p.sh.a + p.sh.g));
+    A.fl = flips_for(p, omegas, rsv::pass_threads_for(p.sh.a + p.sh.g, A.kind, p.sh.a));
     A.dg = diag_for(c, p, deltas);
     A.x = reinterpret_cast<const cplx*>(psi);
     A.x_scale_slot = rsv::SC_ONE;

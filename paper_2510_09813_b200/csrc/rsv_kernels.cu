@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 //   e buf  : this tile's elementwise operand, requested after the same barrier, awaited
 //            just before the epilogue
 template <int TB, int KIND, int NT, bool DIAG>
-__global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kernel_tma(const __grid_constant__ PassArgs A) {
+__global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2) pass_kernel_tma(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 // that load has a whole epilogue plus the next tile's flips to land; the operand buffer of tile it
 // receives x(it+2) after the next tile barrier (A). Cost: one more CTA barrier per tile.
 template <int TB, int KIND, int NT, bool DIAG>
-__global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kernel_rot(const __grid_constant__ PassArgs A) {
+__global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2) pass_kernel_rot(const __grid_constant__ PassArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -1682,16 +1682,30 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   // measured at N=26/29: the prefetched operand pays off in the last pass (its q-sweep leaves
   // less time to hide the operand load); the lo/mid passes are faster without the extra barrier
   if constexpr (TB >= 3 && KIND == PASS_LAST_LANCZOS) {
-    static int occ_rot = 0;
     constexpr size_t smem_rot = 3 * (1 << TB) * sizeof(cplx) + 48 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+    if constexpr (TB == kLoBits && RSV_LAST_THREADS != NT) {
+      if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
+        static int occ_last = 0;
+        return launch_persistent(pass_kernel_rot<TB, KIND, RSV_LAST_THREADS, DIAG>, args, args.sh.n_tiles,
+                                 RSV_LAST_THREADS, smem_rot, &occ_last, st);
+      }
+    }
+    static int occ_rot = 0;
     return launch_persistent(pass_kernel_rot<TB, KIND, NT, DIAG>, args, args.sh.n_tiles, NT, smem_rot, &occ_rot,
                              st);
   }
 #endif
 #if RSV_TMA
   if constexpr (TB >= 3) {
-    static int occ_tma = 0;
     constexpr size_t smem_tma = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+    if constexpr (TB == kLoBits && KIND == PASS_MID && RSV_LAST_THREADS != NT) {
+      if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
+        static int occ_mid = 0;
+        return launch_persistent(pass_kernel_tma<TB, KIND, RSV_LAST_THREADS, DIAG>, args, args.sh.n_tiles,
+                                 RSV_LAST_THREADS, smem_tma, &occ_mid, st);
+      }
+    }
+    static int occ_tma = 0;
     return launch_persistent(pass_kernel_tma<TB, KIND, NT, DIAG>, args, args.sh.n_tiles, NT, smem_tma, &occ_tma,
                              st);
   }

@@ -47,6 +47,17 @@ constexpr int kGcStride = 14;     // lo-pass tile table row: gc[0..11], hh, tb (
 #define RSV_PASS_THREADS 512
 #endif
 constexpr int pass_threads(int tb) { return (1 << tb) < RSV_PASS_THREADS ? (1 << tb) : RSV_PASS_THREADS; }
+// The middle and last Lanczos passes of a full tile may run fewer threads with more amplitudes
+// each (more register bits: fewer shared-memory flips, and in the last pass a cheaper q-sweep),
+// when the contiguous run still fits below the thread bits (a <= log2 threads).
+#ifndef RSV_LAST_THREADS
+#define RSV_LAST_THREADS 256   // measured at N=29: last pass 5.16 -> 5.01 ms (4 register bits)
+#endif
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+constexpr int pass_threads_for(int tb, int kind, int a) {
+  return ((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ? RSV_LAST_THREADS
+                                                                                       : pass_threads(tb);
+}
 constexpr int combine_threads(int tb) { return (1 << tb) < 512 ? (1 << tb) : 512; }
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
