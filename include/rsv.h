@@ -145,6 +145,11 @@ int rsv_set_shard_peers(rsv_context* ctx, int n_global, const void* const* ptrs,
 /* This shard's share of ||psi||^2 from the last Krylov combination / measurement. */
 int rsv_shard_local_norm_sq(rsv_context* ctx, double* out);
 
+/* Full re-orthogonalisation of every new Lanczos vector against the basis (the reference algorithm,
+ * krylov.py:103-104; classical Gram-Schmidt, two extra passes over the basis per iteration). Off by
+ * default: the fused step uses the plain three-term recurrence. */
+int rsv_set_reorthogonalize(rsv_context* ctx, int on);
+
 /* Pass-plan override (tests / tuning): chunk_group_bits -1 = auto (chunk pass at N >= 22), 0 = plain
  * bit-group passes, 3..9 = force the L2-resident chunk pass over bits [0, 12 + g); chunk_lag = M tiles
  * handed out ahead of the first L tile (-1 = auto, 1.5 chunks). No reference counterpart: the reference

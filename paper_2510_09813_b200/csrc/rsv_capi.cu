@@ -51,7 +51,8 @@ int fail(int code, const char* fmt, ...) {
 constexpr double kNsToUs = 1e-3;          // krylov.py:21
 constexpr double kBreakdownRtol = 1e-14;  // krylov.py:25
 constexpr int kScratchJ = 127;            // alpha-partial slot used by plain H.psi
-constexpr int kPartStride = 2 + rsv::kMaxMasks;   // widest partial row (combine)
+constexpr int kPartStride = 2 * rsv::kMaxKrylov > 2 + rsv::kMaxMasks ? 2 * rsv::kMaxKrylov
+                                                                      : 2 + rsv::kMaxMasks;   // widest partial row
 
 // ---------------------------------------------------------------- tridiagonal eigen (implicit QL)
 // Eigen-decomposition of the symmetric tridiagonal (d, e); rotations are
@@ -229,6 +230,8 @@ struct rsv_context {
   // peer-memory mode: the partner shards' slots mapped into this process (CUDA IPC / UVA);
   // peer_slots[g][physical slot] for global qubit g (empty: exchange through the callback)
   std::vector<std::vector<const cplx*>> peer_slots;
+  bool reorth = false;              // full re-orthogonalisation (krylov.py:103-104), opt-in
+  double* d_dots = nullptr;         // <s_i|w> scratch (2 kMaxKrylov doubles)
   int plan_gm = -1;               // chunk group bits: -1 auto, 0 off, 3..9 forced (rsv_set_plan)
   long long plan_lag = -1;        // chunk scheduler lag in M tiles (-1 auto)
   unsigned long long* d_ticket = nullptr;
@@ -800,6 +803,63 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
   return RSV_OK;
 }
 
+// Full re-orthogonalisation of w_j = s_{j+1} against s_0..s_j (krylov.py:103-104, classical
+// Gram-Schmidt: one multi-dot pass, then one Krylov-combination pass that subtracts the projections
+// in place and recomputes ||w||^2 and the q-sweep of the last pass). Returns the new beta_j and
+// rewrites beta_j, sigma_{j+1}, q_{j+1} on the device.
+int reorthogonalize(rsv_context* c, int j, double n0, const std::vector<double>& betas, const double* omegas,
+                    const double* deltas, double* beta_out) {
+  const int k = j + 1;
+  if (k + 1 > rsv::kMaxKrylov) return fail(RSV_ERR_ARG, "re-orthogonalisation of %d vectors exceeds %d", k, rsv::kMaxKrylov - 1);
+  rsv::MultiDotArgs M{};
+  for (int i = 0; i < k; ++i) M.v[i] = slot(c, i);
+  M.w = slot(c, j + 1);
+  M.k = k;
+  M.n = 1ull << c->n;
+  M.part = c->d_part;
+  M.stride = kPartStride;
+  M.counter = c->d_counter;
+  M.out = c->d_dots;
+  CUDA_TRY(rsv::launch_multidot(M, c->st));
+  std::vector<double> dots(2 * k);
+  CUDA_TRY(cudaMemcpyAsync(dots.data(), c->d_dots, sizeof(double) * 2 * k, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  rsv::CombineArgs A{};
+  const PassPlan& last = c->plan.back();
+  A.sh = last.sh;
+  A.qsweep = 1;
+  A.fl = flips_for(last, omegas, rsv::combine_threads(last.sh.a + last.sh.g));
+  A.dg = diag_for(c, last, deltas);
+  A.k = k + 1;
+  A.v[0] = slot(c, j + 1);
+  A.coef[0] = make_double2(1.0, 0.0);
+  for (int i = 0; i < k; ++i) {
+    const double sg = i == 0 ? 1.0 / n0 : 1.0 / betas[i - 1];
+    A.v[i + 1] = slot(c, i);
+    A.coef[i + 1] = make_double2(-sg * sg * dots[2 * i], -sg * sg * dots[2 * i + 1]);
+  }
+  A.out = slot(c, j + 1);   // elementwise: in place
+  A.nmask = 0;
+  A.sc = c->d_sc;
+  A.part = c->d_part;
+  A.counter = c->d_counter;
+  A.sc_out = rsv::SC_GF + 1;
+  prof_begin(c, 3);
+  CUDA_TRY(rsv::launch_combine(A, c->st));
+  prof_end(c);
+  double raw[2];
+  CUDA_TRY(cudaMemcpyAsync(raw, c->d_sc + rsv::SC_GF + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  const double nrm2 = raw[0], beta = std::sqrt(std::max(0.0, nrm2));
+  const double sg = beta > 0.0 ? 1.0 / beta : 0.0, q = nrm2 > 0.0 ? raw[1] / nrm2 : 0.0;
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_BE + j, &beta, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_SG + j + 1, &sg, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_Q + j + 1, &q, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  *beta_out = beta;
+  return RSV_OK;
+}
+
 // One Lanczos run on the resident state for a time step of dt_rest (<= the requested step).
 // Returns the fraction of dt_rest actually advanced (1 when converged on the full step, < 1
 // when the Krylov basis hit the HBM cap and the step was split).
@@ -869,6 +929,10 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
     }
     alphas.push_back(c->h_pin[rsv::SC_AL + j]);
     beta = c->h_pin[rsv::SC_BE + j];
+    if (c->reorth) {
+      rc = reorthogonalize(c, j, n0, betas, omegas, deltas, &beta);
+      if (rc) return rc;
+    }
     y = tridiag_exp_e1(alphas, betas, tau, false);
     residual = beta * std::abs(y.back());
     k = (int)alphas.size();
@@ -1004,6 +1068,7 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
   if (e == cudaSuccess) e = cudaMalloc(&c->d_dl, sizeof(double) << rsv::kLoBits);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_gc, sizeof(double) * rsv::kGcStride * gc_rows);
   const size_t done_rows = n_qubits > 15 ? size_t(1) << (n_qubits - 15) : 1;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dots, sizeof(double) * 2 * rsv::kMaxKrylov);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_ticket, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_done, sizeof(unsigned) * done_rows);
   if (e == cudaSuccess) e = cudaMemset(c->d_ticket, 0, sizeof(unsigned long long));
@@ -1036,6 +1101,7 @@ void rsv_destroy(rsv_context* c) {
   cudaFree(c->d_dl);
   cudaFree(c->d_gc);
   cudaFree(c->d_ticket);
+  cudaFree(c->d_dots);
   cudaFree(c->d_done);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->obs_event) cudaEventDestroy(c->obs_event);
@@ -1377,6 +1443,13 @@ int rsv_set_shard_peers(rsv_context* c, int n_global, const void* const* ptrs, i
 int rsv_shard_local_norm_sq(rsv_context* c, double* out) {
   if (!c || !out) return fail(RSV_ERR_ARG, "NULL argument");
   *out = c->local_n0sq;
+  return RSV_OK;
+}
+
+int rsv_set_reorthogonalize(rsv_context* c, int on) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (on && c->sharded) return fail(RSV_ERR_STATE, "re-orthogonalisation is not available for sharded runs");
+  c->reorth = on != 0;
   return RSV_OK;
 }
 

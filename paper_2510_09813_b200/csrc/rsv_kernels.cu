@@ -1,6 +1,8 @@
 // rsv_kernels.cu -- sm_100a kernels; see rsv_kernels.cuh for the design notes.
 #include "rsv_kernels.cuh"
 
+#include <algorithm>
+
 #ifndef RSV_STAGES
 #define RSV_STAGES 2
 #endif
@@ -1395,6 +1397,11 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __
   }
   if (tid == 0) {
     *A.counter = 0u;
+    if (A.sc_out >= 0) {   // re-orthogonalisation: raw ||w||^2 and <w|A_last|w> to scratch slots
+      A.sc[A.sc_out] = tot[0];
+      A.sc[A.sc_out + 1] = tot[1];
+      return;
+    }
     A.sc[SC_N0SQ] = tot[0];
     if (A.raw) {   // sharded: the host all-reduces ||psi||^2, <psi|A|psi> and the masks, then finishes
       A.sc[SC_Q + 0] = tot[1];
@@ -1619,6 +1626,44 @@ __global__ void sample_kernel(const cplx* __restrict__ psi, uint64_t n, const do
     if (found) break;
   }
   if (lane == 0) out[shot] = result;
+}
+
+// <s_i|w> for i < k (complex), one pass over w and the k vectors; deterministic per-CTA rows
+// (re-orthogonalisation of the fused Lanczos step, krylov.py:103-104).
+__global__ void multidot_kernel(const MultiDotArgs A) {
+  __shared__ double red[32];
+  __shared__ double s_row[2 * kMaxKrylov];
+  const uint64_t n = A.n;
+  for (int i = 0; i < A.k; ++i) {
+    double re = 0.0, im = 0.0;
+    for (uint64_t e = blockIdx.x * (uint64_t)kThreads + threadIdx.x; e < n; e += (uint64_t)gridDim.x * kThreads) {
+      const cplx a = A.v[i][e], b = A.w[e];
+      re = fma(a.x, b.x, fma(a.y, b.y, re));   // conj(a) b
+      im = fma(a.x, b.y, fma(-a.y, b.x, im));
+    }
+    re = block_sum<kThreads>(re, red);
+    im = block_sum<kThreads>(im, red);
+    if (threadIdx.x == 0) {
+      s_row[2 * i] = re;
+      s_row[2 * i + 1] = im;
+    }
+  }
+  const int ncol = 2 * A.k;
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncol; c += kThreads) A.part[(size_t)blockIdx.x * A.stride + c] = s_row[c];
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(A.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < ncol; c += kThreads) {
+    double v = 0.0;
+    for (unsigned r = 0; r < gridDim.x; ++r) v += __ldcg(A.part + (size_t)r * A.stride + c);   // fixed order
+    A.out[c] = v;
+  }
+  if (threadIdx.x == 0) *A.counter = 0u;
 }
 
 __global__ void axpy_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, double2 a, uint64_t n) {
@@ -1877,6 +1922,12 @@ cudaError_t launch_sample(const cplx* psi, uint64_t n, const double* prefix, uin
   const int warps = kThreads / 32;
   const uint64_t blocks = (uint64_t)(shots + warps - 1) / warps;
   sample_kernel<<<(unsigned)blocks, kThreads, 0, st>>>(psi, n, prefix, nchunks, u, total, shots, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_multidot(const MultiDotArgs& args, cudaStream_t st) {
+  // a fixed grid: the reduction rows must fit the partial buffer (max_grid_rows)
+  multidot_kernel<<<(unsigned)std::min<uint64_t>(flat_grid(args.n, 0), (uint64_t)num_sms() * 2), kThreads, 0, st>>>(args);
   return cudaGetLastError();
 }
 

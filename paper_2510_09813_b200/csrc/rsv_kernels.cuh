@@ -148,6 +148,7 @@ struct CombineArgs {
   int nmask;                            // observables: sum_b |psi_b|^2 [b & M == M]
   uint64_t mask[kMaxMasks];
   int raw;                              // sharded run: store local sums (host all-reduces)
+  int sc_out = -1;                      // >= 0: raw ||out||^2, <out|A|out> to sc[sc_out], sc[sc_out+1] only
   int obs_single;                       // every mask is one bit: obs_cat 0 = constant over the tile
   unsigned char obs_cat[kMaxMasks];     //   (obs_pos = global bit), 1 = thread-index bit, 2 = register
   unsigned char obs_pos[kMaxMasks];     //   bit of the thread (obs_pos = that bit's index)
@@ -181,10 +182,20 @@ struct alignas(64) ChunkArgs {
   unsigned* done;                       // per-chunk finished M tiles (reset by the last CTA)
 };
 
+struct MultiDotArgs {
+  const cplx* v[kMaxKrylov];
+  const cplx* w;
+  int k;
+  uint64_t n;
+  double* part; int stride; unsigned* counter;
+  double* out;                          // 2k doubles: <v_i|w> (re, im)
+};
+
 // host-side launchers (rsv_kernels.cu); persistent grids sized from the occupancy query
 cudaError_t launch_pass(const PassArgs& args, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st);
 cudaError_t launch_chunk(const ChunkArgs& args, cudaStream_t st);
+cudaError_t launch_multidot(const MultiDotArgs& args, cudaStream_t st);
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
                             double offset, double* dl, cudaStream_t st);
 cudaError_t launch_global_flip(cplx* u, const cplx* xp, const cplx* x, double c, uint64_t n, double* part,

@@ -79,6 +79,10 @@ class Context:
             out.append(d)
         return out
 
+    def set_reorthogonalize(self, on: bool):
+        """Full re-orthogonalisation of the Lanczos basis (reference krylov.py:103-104), opt-in."""
+        nat.check(self.lib.rsv_set_reorthogonalize(self.ctx, 1 if on else 0), "rsv_set_reorthogonalize")
+
     def set_plan(self, chunk_group_bits: int = -1, chunk_lag: int = -1):
         """Pass-plan override (tests/tuning): -1 auto, 0 plain passes, 3..9 force the chunk pass."""
         nat.check(self.lib.rsv_set_plan(self.ctx, int(chunk_group_bits), int(chunk_lag)), "rsv_set_plan")

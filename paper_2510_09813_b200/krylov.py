@@ -37,6 +37,9 @@ class KrylovConfig:
     tolerance: float = 1e-10
     max_krylov_dim: int = 100
     norm_epsilon: float = 1e-14
+    # extension: re-orthogonalise every Lanczos vector against the basis as the reference does
+    # (krylov.py:103-104); the fused default is the plain three-term recurrence
+    reorthogonalize: bool = False
 
     def __post_init__(self):
         if not 0.0 < self.tolerance <= 1e-1:
@@ -85,6 +88,7 @@ def _fused(slice_, psi, dt_ns, cfg):
         eng.dvec.copy_(_as_device(slice_.diagonal, dtype="float64")[0])
         deltas = np.zeros(n)
     try:
+        eng.set_reorthogonalize(cfg.reorthogonalize)
         eng.set_state(x)
         rep = eng.step(slice_.omegas, deltas, float(dt_ns), cfg.tolerance, cfg.max_krylov_dim, cfg.norm_epsilon)
         out = eng.state().clone()

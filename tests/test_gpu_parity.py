@@ -325,3 +325,38 @@ class TestSampling:
         freq = np.array([((idx >> q) & 1).mean() for q in range(n)])
         sigma = np.sqrt(occ * (1 - occ) / shots) + 1e-12
         assert np.all(np.abs(freq - occ) <= 6 * sigma)
+
+
+class TestReorthogonalization:
+    """KrylovConfig(reorthogonalize=True): the fused step re-orthogonalises every Lanczos vector like
+    the reference (krylov.py:103-104) -- same acceptance bar, iteration counts as the reference's."""
+
+    @pytest.mark.parametrize("case", ["random1", "detmap12", "adiabatic9"])
+    def test_golden_evolutions(self, rs, case):
+        g = load(f"evolve_{case}.npz")
+        n = g["omegas"].shape[1]
+        reg = rs.Register(tuple(map(tuple, g["positions"])), float(g["c6"]))
+        seq = rs.DiscretizedSequence(int(g["dt"]), g["omegas"], g["deltas"], int(g["dt"]) * g["omegas"].shape[0])
+        cfg = rs.SvRunConfig(krylov=rs.KrylovConfig(float(g["tol"]), reorthogonalize=True),
+                             observables=(rs.ObservableSpec("occupation", (), int(g["every"])),))
+        res = rs.evolve_sv(seq, reg, cfg)
+        psi = res.final_state.cpu().numpy()
+        assert 1.0 - abs(np.vdot(g["final_state"], psi)) ** 2 <= 1e-10
+        occ = np.array([r.values for r in res.observables])
+        assert np.abs(occ - g["occ"]).max() <= 1e-8
+        iters = np.array([r.iterations for r in res.krylov_reports])
+        assert np.abs(iters - g["iterations"]).max() <= 1
+
+    @pytest.mark.parametrize("n", [14, 22])
+    def test_matches_plain_recurrence(self, rs, torch, n):
+        rng = np.random.default_rng(n)
+        om, de, u = random_slice(rng, n)
+        s = rs.HamiltonianSlice.from_parameters(om, de, u)
+        psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        psi /= np.linalg.norm(psi)
+        a, ra = rs.expm_multiply(s, psi, 8.0, rs.KrylovConfig(1e-12))
+        b, rb = rs.expm_multiply(s, psi, 8.0, rs.KrylovConfig(1e-12, reorthogonalize=True))
+        assert ra.converged and rb.converged
+        assert np.linalg.norm(a - b) <= 1e-10
+        ref = O.expm_multiply(lambda v: O.apply_hamiltonian(om, O.build_diagonal(de, u), v), psi, 8.0, 1e-12)[0]
+        assert np.linalg.norm(b - ref) <= 1e-10
