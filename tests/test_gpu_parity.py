@@ -360,3 +360,36 @@ class TestReorthogonalization:
         assert np.linalg.norm(a - b) <= 1e-10
         ref = O.expm_multiply(lambda v: O.apply_hamiltonian(om, O.build_diagonal(de, u), v), psi, 8.0, 1e-12)[0]
         assert np.linalg.norm(b - ref) <= 1e-10
+
+
+class TestMaxSize:
+    """N=30, the largest register one B200 holds with a useful Krylov basis (17 GB per vector;
+    plan lo + two 9-bit groups with 128 B runs), through size-independent properties."""
+
+    def test_n30_norm_energy_reversibility(self, rs, torch):
+        from paper_2510_09813_b200 import workloads
+        from paper_2510_09813_b200.engine import SvEngine
+
+        n = 30
+        reg, seq = workloads.config("random29", n_override=n)
+        u = rs.interaction_matrix(reg)
+        eng = SvEngine(n, u, diag="fly", max_krylov_dim=100, krylov_vectors_cap=6)
+        try:
+            plan = eng.pass_plan()
+            assert [p["g"] for p in plan] == [0, 9, 9]
+            for k in range(6):
+                rep = eng.step(*seq.step(k), 10.0, 1e-10, 100, next_params=seq.step(k + 1))
+                assert rep.converged
+            om, de = seq.step(6)
+            psi0 = eng.state().clone()
+            rep = eng.step(om, de, 10.0, 1e-10, 100)
+            assert rep.converged and rep.substeps >= 1          # 6 resident vectors: split steps
+            assert abs(math.sqrt(rs.overlap(eng.state(), eng.state()).real) - 1.0) <= 1e-9
+            back = eng.step(om, de, -10.0, 1e-10, 100)
+            assert back.converged
+            assert rs.norm_difference(eng.state(), psi0) <= 1e-8
+            assert abs(back.alpha0 - rep.alpha0) <= 1e-9 * max(1.0, abs(rep.alpha0))   # energy conserved
+        finally:
+            eng.close()
+            del eng
+            torch.cuda.empty_cache()
