@@ -22,6 +22,9 @@
 #ifndef RSV_QSWEEP_OFF
 #define RSV_QSWEEP_OFF 0
 #endif
+#ifndef RSV_ROT_MID
+#define RSV_ROT_MID 0
+#endif
 // rotating tile buffers: the elementwise operand is prefetched one tile ahead too (pass_kernel_rot)
 #ifndef RSV_ROT
 #define RSV_ROT 1
@@ -1726,7 +1729,7 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
 #if RSV_TMA && RSV_ROT
   // measured at N=26/29: the prefetched operand pays off in the last pass (its q-sweep leaves
   // less time to hide the operand load); the lo/mid passes are faster without the extra barrier
-  if constexpr (TB >= 3 && KIND == PASS_LAST_LANCZOS) {
+  if constexpr (TB >= 3 && (KIND == PASS_LAST_LANCZOS || (RSV_ROT_MID && KIND == PASS_MID))) {
     constexpr size_t smem_rot = 3 * (1 << TB) * sizeof(cplx) + 48 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
     if constexpr (TB == kLoBits && RSV_LAST_THREADS != NT) {
       if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
