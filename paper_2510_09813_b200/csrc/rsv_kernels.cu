@@ -1208,7 +1208,7 @@ __global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ Ch
 // q_0 (q-sweep with the next step's coefficients) and the observable masks. Observables
 // are reduced per warp into shared rows (no block barriers inside the tile loop).
 template <int TB, int NT>
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) combine_kernel(const __grid_constant__ CombineArgs A) {
+__global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine_kernel(const __grid_constant__ CombineArgs A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;

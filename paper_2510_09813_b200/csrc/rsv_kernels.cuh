@@ -58,7 +58,10 @@ constexpr int pass_threads_for(int tb, int kind, int a) {
   return ((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ? RSV_LAST_THREADS
                                                                                        : pass_threads(tb);
 }
-constexpr int combine_threads(int tb) { return (1 << tb) < 512 ? (1 << tb) : 512; }
+#ifndef RSV_COMBINE_THREADS
+#define RSV_COMBINE_THREADS 512
+#endif
+constexpr int combine_threads(int tb) { return (1 << tb) < RSV_COMBINE_THREADS ? (1 << tb) : RSV_COMBINE_THREADS; }
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
 // scalar slots (device double array, reset per step)
