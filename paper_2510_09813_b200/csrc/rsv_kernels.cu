@@ -1706,9 +1706,15 @@ unsigned flat_grid(uint64_t n, int grid) {
 }
 
 // Launch with grid = min(tiles, SMs x resident CTAs); the occupancy query is done once per kernel.
+// Experiment switch: grid of the HBM-bound lo pass (0 = one CTA per SM); fewer CTAs draw less
+// power under the 1 kW cap, which the SM-bound passes could use as clock.
+#ifndef RSV_GRID_LO
+#define RSV_GRID_LO 0
+#endif
+
 template <typename Kernel, typename Args>
 cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, int nt, size_t smem, int* occ_cache,
-                              cudaStream_t st) {
+                              cudaStream_t st, unsigned grid_cap = 0) {
   if (*occ_cache == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1717,7 +1723,8 @@ cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, in
     if (e != cudaSuccess) return e;
     *occ_cache = occ > 0 ? occ : 1;
   }
-  const uint64_t cap = (uint64_t)num_sms() * (uint64_t)*occ_cache;
+  uint64_t cap = (uint64_t)num_sms() * (uint64_t)*occ_cache;
+  if (grid_cap > 0 && grid_cap < cap) cap = grid_cap;
   const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
   kern<<<grid, nt, smem, st>>>(args);
   return cudaGetLastError();
@@ -1755,7 +1762,7 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
     }
     static int occ_tma = 0;
     return launch_persistent(pass_kernel_tma<TB, KIND, NT, DIAG>, args, args.sh.n_tiles, NT, smem_tma, &occ_tma,
-                             st);
+                             st, (KIND == PASS_FIRST && DIAG) ? RSV_GRID_LO : 0u);
   }
 #endif
   constexpr int STAGES = TB >= 8 ? RSV_STAGES : 2;
