@@ -785,9 +785,13 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
       A.ein_is_prev = 0;
     }
     A.out = slot(c, j + 1);   // u in place, then s_{j+1}
-    if (p2p && pi == 0) {
+    if (p2p && !last) {
+      // the partner reads (NVLink) are spread over the passes before the last one so they overlap
+      // more local work: active global qubit number i goes to pass i mod (np - 1)
+      int active = 0;
       for (size_t g = 0; g < c->gcoef.size(); ++g) {
         if (c->gcoef[g] == 0.0) continue;
+        if (active++ % (int)(np - 1) != (int)pi) continue;
         A.peer[A.npeer] = c->peer_slots[g][c->logical[j]];
         A.peer_coef[A.npeer] = c->gcoef[g];
         ++A.npeer;

@@ -55,15 +55,16 @@ def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False):
 @pytest.mark.timeout(400)
 @pytest.mark.parametrize("world,n,cap,peer", [(2, 14, None, False), (4, 14, None, False), (2, 17, None, False),
                                               (2, 14, 6, False), (2, 17, None, True), (4, 16, None, True),
-                                              (2, 15, 6, True)])
+                                              (2, 15, 6, True), (4, 24, None, True)])
 def test_fused_sharded_evolution(tmp_path, world, n, cap, peer):
     # (4, 14): 12 local qubits -> one lo pass carries the diagonal, the shard offset and the q-sweep;
     # (2, 17): 16 local qubits -> lo + one group pass; cap 6 forces exact sub-stepping across shards;
-    # peer=True: peer-memory mode (the first pass reads the partner shards' slots through CUDA IPC --
-    # here on the same device, over NVLink on a multi-GPU box)
+    # peer=True: peer-memory mode (the first passes read the partner shards' slots through CUDA IPC --
+    # here on the same device, over NVLink on a multi-GPU box); (4, 24): 22 local qubits, three passes,
+    # the two global qubits' partner reads split over the lo and mid passes
     import torch.multiprocessing as mp
 
-    k0, steps = 30, 4
+    k0, steps = 30, (4 if n < 20 else 1)   # the CPU oracle pays 2^n per H.psi with full re-orthogonalisation
     mp.spawn(_worker, args=(world, _port(), str(tmp_path), n, k0, steps, cap, peer), nprocs=world, join=True)
     psi = np.concatenate([np.load(tmp_path / f"s{r}.npy") for r in range(world)])
     inp = np.load(tmp_path / "in.npy", allow_pickle=True).item()
