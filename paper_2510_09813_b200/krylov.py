@@ -88,7 +88,7 @@ def _fused(slice_, psi, dt_ns, cfg):
         eng.dvec.copy_(_as_device(slice_.diagonal, dtype="float64")[0])
         deltas = np.zeros(n)
     try:
-        eng.set_reorthogonalize(cfg.reorthogonalize)
+        eng.set_reorthogonalize(getattr(cfg, "reorthogonalize", False))   # absent on the reference's config
         eng.set_state(x)
         rep = eng.step(slice_.omegas, deltas, float(dt_ns), cfg.tolerance, cfg.max_krylov_dim, cfg.norm_epsilon)
         out = eng.state().clone()

@@ -82,3 +82,18 @@ def test_execute_run_matches_reference(case):
         assert a["t_ns"] == b["t_ns"]
         assert np.abs(np.array(a["re"]) + 1j * np.array(a["im"]) - np.array(b["re"]) - 1j * np.array(b["im"])).max() <= 1e-8
     assert doc["samples"] == ref["samples"]
+
+
+def test_foreign_observable_specs_are_accepted():
+    # rydsim's ObservableSpec objects (or anything with its fields) pass through evolve_sv unchanged
+    from types import SimpleNamespace
+
+    import paper_2510_09813_b200 as rs
+    from paper_2510_09813_b200.sv import as_spec
+
+    spec = as_spec(SimpleNamespace(kind="correlation", qubits=[0, 1, 2, 3], every_n_steps=0))
+    assert isinstance(spec, rs.ObservableSpec) and spec.qubits == (0, 1, 2, 3) and spec.every_n_steps == 0
+    mine = rs.ObservableSpec("occupation", (1,), 2)
+    assert as_spec(mine) is mine
+    with pytest.raises(rs.ValidationError):
+        as_spec(SimpleNamespace(kind="entropy", qubits=(), every_n_steps=1))
