@@ -60,7 +60,7 @@ int rsv_set_stream(rsv_context* ctx, void* stream);
  * sums in slot j+1 and turns them into s_{j+1} in place, so the last slot needs no basis vector.
  * The Krylov cap is nslots - 1 vectors; steps needing more are split (exactly) in time. */
 int rsv_bind_slots(rsv_context* ctx, void* const* slots, int nslots);
-/* Index of the bound slot currently holding the state (changes after every step). */
+/* Index of the bound slot holding the state (slot 0: the Krylov combination writes it in place). */
 int rsv_state_slot(rsv_context* ctx, int* out);
 /* Bind a caller-allocated device buffer of 2^n float64 used as the diagonal vector:
  * if fill_interaction != 0 it is filled with sum_{i<j} U_ij n_i n_j (sv.py:116),
@@ -100,13 +100,13 @@ int rsv_measure(rsv_context* ctx, double* out_host, double* norm_sq);
 /* Same masks on an arbitrary device vector psi (read-only), e.g. observables.occupations(). */
 int rsv_observe(rsv_context* ctx, const void* psi, const uint64_t* masks, int nmask, double* out_host,
                 double* norm_sq);
-/* sum_b |x_b - y_b|^2 (observables.py:137 norm_difference, computed without cancellation). */
 /* Basis-state indices drawn from |psi|^2 by inverse CDF (replaces observables.py:167 sample_bitstrings,
  * dense path): `uniforms` are the reference's per-batch PCG64 draws (host), out_indices[s] = the first
  * index whose cumulative |psi|^2 exceeds uniforms[s] * ||psi||^2 (searchsorted side="right"; cdf[-1] = 1).
  * norm_sq (may be NULL) returns ||psi||^2 for the caller's normalisation check. psi has 2^n amplitudes. */
 int rsv_sample(rsv_context* ctx, const void* psi, const double* uniforms, int64_t shots, int64_t* out_indices,
                double* norm_sq);
+/* sum_b |x_b - y_b|^2 (observables.py:137 norm_difference, computed without cancellation). */
 int rsv_diff_norm_sq(rsv_context* ctx, const void* x, const void* y, uint64_t n, double* out);
 
 /* Generic vector kernels for the callable-matvec Lanczos (krylov.py:96-121). */
