@@ -19,6 +19,9 @@
 #include "rsv.h"
 #include "rsv_kernels.cuh"
 
+#ifndef RSV_L2_PROMOTION
+#define RSV_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B   // strided tile loads pull whole 256 B sectors
+#endif
 #ifndef RSV_TENSOR_MAPS
 #define RSV_TENSOR_MAPS 1   // 5-D TMA descriptors for the strided tiles (0: per-warp bulk runs)
 #endif
@@ -171,7 +174,7 @@ bool encode_tile_map(CUtensorMap* m, const void* base, const rsv::Shape& sh) {
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dim, stride, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        (CUtensorMapL2promotion)RSV_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
