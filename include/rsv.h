@@ -142,6 +142,9 @@ int rsv_set_shard_step(rsv_context* ctx, double offset, double next_offset, int 
  * directly (P2P loads) instead of exchanging copies; n_global = 0 returns to the exchange mode.
  * Plans with a single pass keep the exchange. */
 int rsv_set_shard_peers(rsv_context* ctx, int n_global, const void* const* ptrs, int nslots);
+/* Make a (mapped) device pointer of another GPU readable from kernels on the current device
+ * (cudaDeviceEnablePeerAccess; a no-op on the same device). */
+int rsv_enable_peer_access(const void* ptr);
 /* This shard's share of ||psi||^2 from the last Krylov combination / measurement. */
 int rsv_shard_local_norm_sq(rsv_context* ctx, double* out);
 

@@ -1428,6 +1428,26 @@ int rsv_set_shard_step(rsv_context* c, double offset, double next_offset, int n_
   return RSV_OK;
 }
 
+int rsv_enable_peer_access(const void* ptr) {
+  if (ptr == nullptr) return fail(RSV_ERR_ARG, "NULL pointer");
+  cudaPointerAttributes at{};
+  CUDA_TRY(cudaPointerGetAttributes(&at, ptr));
+  if (at.type != cudaMemoryTypeDevice) return fail(RSV_ERR_ARG, "not a device pointer");
+  int cur = 0;
+  CUDA_TRY(cudaGetDevice(&cur));
+  if (at.device == cur) return RSV_OK;
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, cur, at.device));
+  if (!can) return fail(RSV_ERR_CUDA, "device %d cannot access device %d's memory (no P2P)", cur, at.device);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();   // clear the non-sticky status
+    return RSV_OK;
+  }
+  if (e != cudaSuccess) return fail(RSV_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d): %s", at.device, cudaGetErrorString(e));
+  return RSV_OK;
+}
+
 int rsv_set_shard_peers(rsv_context* c, int n_global, const void* const* ptrs, int nslots) {
   if (!c) return fail(RSV_ERR_ARG, "NULL context");
   if (n_global == 0 || ptrs == nullptr) {

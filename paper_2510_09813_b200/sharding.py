@@ -411,7 +411,10 @@ class FusedShardEngine:
                 tensors = [fn(*args) for fn, args in everyone[peer]]
                 self._peer_tensors.append(tensors)
                 table.extend(t.data_ptr() for t in tensors)
-        except Exception:   # pragma: no cover - platform without CUDA IPC
+            with torch.cuda.device(self.device):   # kernels on this GPU read the partners' memory
+                for p in table[:: len(self.eng.slots)]:
+                    nat.check(self.eng.lib.rsv_enable_peer_access(p), "rsv_enable_peer_access")
+        except Exception:   # pragma: no cover - platform without CUDA IPC / P2P
             ok = 0.0
         flag = torch.tensor([ok], dtype=torch.float64, device=self.device if self.nccl else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
