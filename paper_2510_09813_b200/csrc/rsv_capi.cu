@@ -296,7 +296,7 @@ constexpr int kDelegateLow = RSV_DELEGATE_LOW;
 int chunk_gm_for(int n, int setting) {
   if (setting == 0) return 0;
   // M tiles keep a = 12 - gm <= log2(pass threads) so a thread's amplitudes sit at one stride
-  const int gmin = std::max(3, rsv::kLoBits - rsv::ilog2(rsv::pass_threads(rsv::kLoBits)));
+  const int gmin = std::max(3, rsv::kLoBits - rsv::ilog2(RSV_CHUNK_THREADS));
   if (setting > 0) return (setting >= gmin && setting <= 9 && n - rsv::kLoBits - setting >= 1) ? setting : 0;
   // auto: off. Measured at N=29 ("L2-resident chunk pass"): the chunk pass cuts a
   // Lanczos iteration's HBM bytes from 144 to 96 per amplitude, but its two tile passes stay
@@ -693,7 +693,7 @@ int launch_chunk_pass(rsv_context* c, const PassPlan& p, const double* omegas, c
   pm.sh = p.shm;
   pm.qubits = p.qubits_m;
   pm.lo = false;
-  const int nt = rsv::pass_threads(rsv::kLoBits);
+  const int nt = RSV_CHUNK_THREADS;
   A.flm = flips_for(pm, omegas, nt);
   A.fll = flips_for(p, omegas, nt);
   A.dg = diag_for(c, p, deltas);
@@ -1486,7 +1486,7 @@ int rsv_set_plan(rsv_context* c, int chunk_group_bits, long long chunk_lag) {
     return fail(RSV_ERR_ARG, "chunk_group_bits must be -1 (auto), 0 (off) or 3..9, got %d", chunk_group_bits);
   if (chunk_group_bits > 0 && chunk_gm_for(c->n, chunk_group_bits) == 0)
     return fail(RSV_ERR_ARG, "chunk group of %d bits is invalid at N=%d (needs M tiles of <= 2^%d contiguous and a hi pass)",
-                chunk_group_bits, c->n, rsv::ilog2(rsv::pass_threads(rsv::kLoBits)));
+                chunk_group_bits, c->n, rsv::ilog2(RSV_CHUNK_THREADS));
   CUDA_TRY(cudaStreamSynchronize(c->st));
   c->plan_gm = chunk_group_bits;
   c->plan_lag = chunk_lag;

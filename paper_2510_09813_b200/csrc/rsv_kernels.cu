@@ -1795,7 +1795,7 @@ cudaError_t launch_pass_tb(const PassArgs& args, cudaStream_t st) {
 
 template <bool DIAG>
 cudaError_t launch_chunk_d(const ChunkArgs& args, cudaStream_t st) {
-  constexpr int NT = pass_threads(kLoBits);
+  constexpr int NT = RSV_CHUNK_THREADS;
   static int occ = 0;
   constexpr size_t smem = 3 * (1 << kLoBits) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
   // tiles are handed out dynamically: the grid only needs to be resident (persistent)

@@ -54,6 +54,10 @@ constexpr int pass_threads(int tb) { return (1 << tb) < RSV_PASS_THREADS ? (1 <<
 #define RSV_LAST_THREADS 256   // measured at N=29: last pass 5.16 -> 5.01 ms (4 register bits)
 #endif
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+// threads of the L2 chunk pass (its M tiles need 12 - gm <= log2 of this)
+#ifndef RSV_CHUNK_THREADS
+#define RSV_CHUNK_THREADS RSV_PASS_THREADS
+#endif
 constexpr int pass_threads_for(int tb, int kind, int a) {
   return ((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ? RSV_LAST_THREADS
                                                                                        : pass_threads(tb);
