@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
   constexpr int RB = RegBits<EPT>::value;
   constexpr int STAGES = TB >= 8 ? RSV_STAGES : 2;
   constexpr bool LANCZOS = KIND == PASS_LAST_LANCZOS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   cplx* sbuf = reinterpret_cast<cplx*>(smem_raw);   // STAGES x TILE
   __shared__ double red[32];
 
@@ -1213,7 +1213,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
   constexpr int NW = (NT + 31) / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   cplx* s = reinterpret_cast<cplx*>(smem_raw);
   __shared__ double red[32];
   __shared__ double s_obs[NW][kMaxMasks];
