@@ -293,7 +293,7 @@ def run_sharded(args, rank, world, local, pg):
     u = interaction_matrix(reg)
     t_setup = time.time()
     eng = FusedShardEngine(n_tot, u, dist, device=torch.device("cuda", local), max_krylov_dim=cfg.max_krylov_dim,
-                           peer_memory=not args.no_peer_memory)
+                           peer_memory=not args.no_peer_memory, krylov_vectors_cap=args.krylov_cap)
     peer_mode = eng.peer_memory
     stream = torch.cuda.current_stream()
 
@@ -334,6 +334,7 @@ def run_sharded(args, rank, world, local, pg):
     krylov_cap = eng.eng.krylov_cap
     eng.close()
     del eng
+    torch.cuda.ipc_collect()
     torch.cuda.empty_cache()
 
     e2e = None
@@ -348,7 +349,8 @@ def run_sharded(args, rank, world, local, pg):
         t0 = time.perf_counter()
         psi, reps2, _occ = evolve_sv_sharded_fused(sub, reg, dist, tolerance=cfg.tolerance,
                                                    device=torch.device("cuda", local), initial_local=host_in,
-                                                   peer_memory=not args.no_peer_memory)
+                                                   peer_memory=not args.no_peer_memory,
+                                                   krylov_vectors_cap=args.krylov_cap)
         host_out.copy_(psi)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t0), pg)
@@ -581,6 +583,9 @@ def main(argv=None):
                     help="pass plan: -1 auto, 0 plain bit-group passes, 3..9 L2 chunk pass (A/B runs)")
     ap.add_argument("--total-qubits", type=int, default=None,
                     help="N > 1: strong scaling of a fixed register (BASELINE configs[4]: 33) instead of n + log2 P")
+    ap.add_argument("--krylov-cap", type=int, default=None,
+                    help="N > 1: resident Krylov vectors per rank (default: what fits; smoke runs of several "
+                         "ranks on one GPU need a cap)")
     ap.add_argument("--no-peer-memory", action="store_true",
                     help="N > 1: exchange the partner shards' vectors instead of reading them over NVLink")
     ap.add_argument("--replicas", action="store_true",

@@ -509,6 +509,12 @@ class FusedShardEngine:
         self.nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self.nat.COMM_FN(), None, None))
         self.dist.barrier()   # partners may still read this shard's slots until everyone is done
         self._peer_tensors = []
+        if self.peer_memory:
+            import gc
+
+            gc.collect()
+            self.dist.barrier()           # every rank has dropped its mappings of the others' slots
+            self.torch.cuda.ipc_collect()  # so the exported blocks can really be freed
         self.eng.close()
 
 
