@@ -163,3 +163,18 @@ class TestSampling:
         a = rs.sample_bitstrings(psi, 10_000, 99)
         assert np.array_equal(a, rs.sample_bitstrings(psi, 10_000, 99))
         assert np.array_equal(a, O.sample_bitstrings(psi, 10_000, 99))
+
+
+def test_snapshots_at_full_size(rs):
+    # N=29: the Krylov workspace takes all of HBM, snapshots go to host memory
+    from paper_2510_09813_b200 import workloads
+
+    reg, seq = workloads.config("random29")
+    sub = rs.DiscretizedSequence(seq.dt_ns, seq.omegas[:2], seq.deltas[:2], 2 * seq.dt_ns)
+    res = rs.evolve_sv(sub, reg, rs.SvRunConfig(snapshot_every=1))
+    assert [t for t, _ in res.snapshots] == [10.0, 20.0]
+    last = res.snapshots[-1][1]
+    assert isinstance(last, np.ndarray) and last.shape == (2 ** 29,)
+    assert abs(np.vdot(last[:2 ** 20], last[:2 ** 20]).real) <= 1.0 + 1e-9
+    # the workspace still holds all of HBM: compare on the host
+    assert np.array_equal(res.final_state[: 2 ** 24].cpu().numpy(), last[: 2 ** 24])
