@@ -176,5 +176,8 @@ def test_snapshots_at_full_size(rs):
     last = res.snapshots[-1][1]
     assert isinstance(last, np.ndarray) and last.shape == (2 ** 29,)
     assert abs(np.vdot(last[:2 ** 20], last[:2 ** 20]).real) <= 1.0 + 1e-9
-    # the workspace still holds all of HBM: compare on the host
+    # the workspace still holds all of HBM: compare on the host, then release it
     assert np.array_equal(res.final_state[: 2 ** 24].cpu().numpy(), last[: 2 ** 24])
+    psi = res.release()
+    assert psi.is_cuda and tuple(psi.shape) == (2 ** 29,) and res.engine is None
+    assert rs.norm_difference(psi, last) == 0.0   # now there is room for other GPU work
