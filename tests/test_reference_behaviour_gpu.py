@@ -181,3 +181,20 @@ def test_snapshots_at_full_size(rs):
     psi = res.release()
     assert psi.is_cuda and tuple(psi.shape) == (2 ** 29,) and res.engine is None
     assert rs.norm_difference(psi, last) == 0.0   # now there is room for other GPU work
+
+
+def test_expm_multiply_at_full_size(rs):
+    # one fused Lanczos step on a user-owned N=29 vector: the workspace leaves room for the result
+    import torch
+
+    from paper_2510_09813_b200 import workloads
+
+    reg, seq = workloads.config("random29")
+    s = rs.HamiltonianSlice.from_parameters(*seq.step(40), rs.interaction_matrix(reg))
+    psi = torch.zeros(2 ** 29, dtype=torch.complex128, device="cuda")
+    psi[0] = 1.0
+    out, rep = rs.expm_multiply(s, psi, 10.0, rs.KrylovConfig(1e-10))
+    assert rep.converged and tuple(out.shape) == (2 ** 29,)
+    assert abs(math.sqrt(rs.overlap(out, out).real) - 1.0) <= 1e-9
+    del out, psi
+    torch.cuda.empty_cache()
