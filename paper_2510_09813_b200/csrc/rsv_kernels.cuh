@@ -11,12 +11,14 @@
 //   * the lo pass: tile = bits [0, a) contiguous (a = min(N, 12)); applies the
 //     flips on those bits plus the diagonal (on the fly from U, or from a
 //     precomputed vector);
-//   * hi passes: tile = 2^a contiguous amplitudes (64..512 B runs, full DRAM
-//     bursts) x 2^g amplitudes strided along a group of g high bits; applies
-//     the flips on the group.
-// A tile is loaded once with cp.async into shared memory; each partner of a
-// flip is then one 16-byte shared load (bank-conflict free: e ^ mask permutes
-// aligned groups of 8 lanes).
+//   * hi passes: tile = 2^a contiguous amplitudes (128..512 B runs) x 2^g
+//     amplitudes strided along a group of g high bits; applies the flips on
+//     the group (the first also the lowest bits, which its tile holds too).
+// A tile is moved once into shared memory by the TMA engine (one bulk copy for a
+// contiguous tile, a 5-D tensor map for a strided one, completion on mbarriers);
+// each partner of a flip is then one 16-byte shared load (bank-conflict free:
+// e ^ mask permutes aligned groups of 8 lanes), flips on a thread's own register
+// bits are register permutations.
 //
 // The Lanczos recurrence is fused into the passes (no separate vdot/axpy/norm
 // passes): the first/middle passes reduce their part of alpha_j = <v_j|H|v_j>,
