@@ -6,14 +6,16 @@ A bench *step* is one exact time step psi <- exp(-i dt H_k) psi (one rsv_expm_st
 Lanczos H.psi passes + Krylov combination + occupation reduction, and the host read of that
 step's occupations). Default: W=3 warm-up steps then K=97 timed steps = the whole 1 us pulse.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 29] [--diag fly|vec]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--qubits 29] [--diag fly|vec]
+                  [--workload random29|lattice27|lattice20|ring10] [--plan-gm G] [--total-qubits 33]
 
 value = H.psi products per second (whole job); ms_per_step; s_per_us_pulse; effective HBM
 GB/s (32 B per amplitude per H.psi: read psi, write H psi); roofline of the dominant kernel;
 e2e through the public API (evolve_sv) with host initial/final state; CPU baseline (C port of
 the reference's numba matvec, OpenMP on the host cores, bounded sample). Multi-GPU (torchrun, P GPUs):
-one register of N = n + log2(P) qubits sharded by its top qubits (weak scaling; run_sharded), max
-over ranks; --replicas runs P independent single-GPU copies instead.
+one register of N = n + log2(P) qubits sharded by its top qubits (weak scaling; run_sharded; the
+partner shards are read with P2P loads unless --no-peer-memory), max over ranks; --total-qubits
+fixes N (strong scaling, BASELINE configs[4]); --replicas runs P independent single-GPU copies.
 """
 
 from __future__ import annotations
