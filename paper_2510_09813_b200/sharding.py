@@ -354,6 +354,13 @@ class FusedShardEngine:
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
+        # bring up the communicator before the workspace takes the GPU's memory (NCCL allocates
+        # its buffers lazily at the first collective / the first pairwise exchange), and leave it
+        # a few GB: the Krylov slots otherwise take all of HBM
+        dist.barrier()
+        if memory_budget_bytes is None:
+            free, _total = torch.cuda.mem_get_info(dev)
+            memory_budget_bytes = max(0, free - (4 << 30))
         self.eng = SvEngine(nl, self.u[:nl, :nl], diag="fly", max_krylov_dim=max_krylov_dim, device=dev,
                             memory_budget_bytes=memory_budget_bytes, krylov_vectors_cap=krylov_vectors_cap)
         self.nccl = dist.get_backend() == "nccl"
