@@ -22,6 +22,10 @@
 #ifndef RSV_QSWEEP_OFF
 #define RSV_QSWEEP_OFF 0
 #endif
+// Krylov combination ring filled by per-warp bulk copies (TMA) instead of per-thread cp.async
+#ifndef RSV_COMBINE_TMA
+#define RSV_COMBINE_TMA 0
+#endif
 #ifndef RSV_ROT_MID
 #define RSV_ROT_MID 0
 #endif
@@ -1241,6 +1245,44 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
   const int kv = A.k;
   uint64_t is_t = blockIdx.x;   // next (tile, vector, stage) to request
   int is_v = 0, is_s = 0;
+#if RSV_COMBINE_TMA
+  // TMA variant: each warp's amplitudes arrive by bulk copies of their contiguous runs, completion
+  // on a per-warp mbarrier per stage (no LSU traffic for the copies; the ring stays warp-private)
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(s + RING * TILE);   // [RING][NW]
+  const int R = (1 << A.sh.a) < 32 ? (1 << A.sh.a) : (NT < 32 ? NT : 32);
+  const int RUNS = (NT < 32 ? NT : 32) / R;
+  const unsigned warp_bytes = (unsigned)((NT < 32 ? NT : 32) * EPT * sizeof(cplx));
+  if (lane == 0)
+    for (int st = 0; st < RING; ++st) mbar_init(&wbar[st * NW + warp], 1);
+  mbar_init_fence();
+  __syncthreads();
+  unsigned wphase = 0u;
+  auto issue_next = [&]() {
+    if (is_t < A.sh.n_tiles) {
+      uint64_t* bar = &wbar[is_s * NW + warp];
+      __syncwarp();                 // the warp is done with this stage's previous contents
+      fence_proxy_async_smem();
+      if (lane == 0) mbar_arrive_expect_tx(bar, warp_bytes);
+      __syncwarp();
+      if (lane < RUNS) {
+        const uint32_t e0 = (uint32_t)(warp * 32 + lane * R);
+        const cplx* src = A.v[is_v] + tile_index(A.sh, is_t, e0);
+        cplx* dst = s + is_s * TILE + e0;
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) bulk_g2s(dst + i * NT, src + off[i], R * sizeof(cplx), bar);
+      }
+      if (++is_v == kv) {
+        is_v = 0;
+        is_t += G;
+      }
+    }
+    is_s = is_s == RING - 1 ? 0 : is_s + 1;
+  };
+  auto wait_item = [&](int st) {
+    mbar_wait(&wbar[st * NW + warp], (wphase >> st) & 1u);
+    wphase ^= 1u << st;
+  };
+#else
   auto issue_next = [&]() {
     if (is_t < A.sh.n_tiles) {
       const cplx* src = A.v[is_v] + tile_index(A.sh, is_t, tid);
@@ -1255,6 +1297,8 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
     cp_async_commit();
     is_s = is_s == RING - 1 ? 0 : is_s + 1;
   };
+  auto wait_item = [&](int) { cp_async_wait<1>(); };   // this item landed; the next may be in flight
+#endif
   issue_next();
   issue_next();
   int stage = 0;
@@ -1265,7 +1309,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
     for (int i = 0; i < EPT; ++i) wv[i] = make_double2(0.0, 0.0);
     int qstage = 0;
     for (int k = 0; k < kv; ++k) {
-      cp_async_wait<1>();   // this item landed; the next one may still be in flight
+      wait_item(stage);
       const cplx* src = s + stage * TILE + tid;
       const double2 c = A.coef[k];
       #pragma unroll
@@ -1347,7 +1391,9 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
     }
   }
 
+#if !RSV_COMBINE_TMA
   cp_async_wait<0>();
+#endif
   double mine[2];
   mine[0] = block_sum<NT>(acc_n, red);
   mine[1] = block_sum<NT>(acc_q, red);
@@ -1806,7 +1852,8 @@ template <int TB>
 cudaError_t launch_combine_tb(const CombineArgs& args, cudaStream_t st) {
   constexpr int NT = combine_threads(TB);
   static int occ = 0;
-  return launch_persistent(combine_kernel<TB, NT>, args, args.sh.n_tiles, NT, 3 * (1 << TB) * sizeof(cplx), &occ, st);
+  return launch_persistent(combine_kernel<TB, NT>, args, args.sh.n_tiles, NT,
+                           3 * (1 << TB) * sizeof(cplx) + (RSV_COMBINE_TMA ? 3 * 32 * sizeof(uint64_t) : 0), &occ, st);
 }
 
 }  // namespace
