@@ -9,6 +9,10 @@
  * with the same per-element arithmetic, parallelised over b with OpenMP
  * (element results do not depend on evaluation order across b).
  * svref_build_diagonal restates hamiltonian.py:83-122 (doubling construction).
+ * svref_zdotc / svref_zaxpy / svref_zscal / svref_norm2 are the vector operations of the
+ * reference's Lanczos loop (krylov.py:96-122: np.vdot, w -= c v, w / beta, np.linalg.norm),
+ * in place and OpenMP-parallel so the oracle can run that loop at N = 27..30 on the host
+ * (oracle/big.py) without numpy temporaries.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -92,4 +96,45 @@ void svref_fill(int64_t count, double* x, uint64_t seed) {
     z ^= z >> 31;
     x[i] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
   }
+}
+
+/* <x|y> = sum conj(x_b) y_b over n complex values (np.vdot, krylov.py:101,104). */
+void svref_zdotc(int64_t n, const double* x, const double* y, double* out2) {
+  double re = 0.0, im = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : re, im)
+  for (int64_t b = 0; b < n; ++b) {
+    const double xr = x[2 * b], xi = x[2 * b + 1], yr = y[2 * b], yi = y[2 * b + 1];
+    re += xr * yr + xi * yi;
+    im += xr * yi - xi * yr;
+  }
+  out2[0] = re;
+  out2[1] = im;
+}
+
+/* y += (a_re + i a_im) x (the in-place form of w -= c v, krylov.py:102-104,119-121). */
+void svref_zaxpy(int64_t n, double a_re, double a_im, const double* x, double* y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < n; ++b) {
+    const double xr = x[2 * b], xi = x[2 * b + 1];
+    y[2 * b] += a_re * xr - a_im * xi;
+    y[2 * b + 1] += a_re * xi + a_im * xr;
+  }
+}
+
+/* y = (a_re + i a_im) x; x may alias y (w / beta, krylov.py:98,119). */
+void svref_zscal(int64_t n, double a_re, double a_im, const double* x, double* y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < n; ++b) {
+    const double xr = x[2 * b], xi = x[2 * b + 1];
+    y[2 * b] = a_re * xr - a_im * xi;
+    y[2 * b + 1] = a_re * xi + a_im * xr;
+  }
+}
+
+/* sum |x_b|^2 (np.linalg.norm squared, krylov.py:93,105). */
+double svref_norm2(int64_t n, const double* x) {
+  double s = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : s)
+  for (int64_t b = 0; b < 2 * n; ++b) s += x[b] * x[b];
+  return s;
 }

@@ -9,6 +9,7 @@ whose arithmetic runs in hand-written sm_100a kernels behind the C ABI in
 __version__ = "0.1.0"
 
 from .errors import (  # noqa: F401
+    REFERENCE_ERRORS,
     ConfigurationError,
     MemoryBudgetError,
     RydsimError,
@@ -21,7 +22,9 @@ from .hamiltonian import (  # noqa: F401
     apply_hamiltonian,
     build_dense,
     build_diagonal,
+    interaction_diagonal,
     interaction_matrix,
+    weighted_bit_sum,
 )
 from .krylov import KrylovConfig, KrylovReport, expm_multiply  # noqa: F401
 from .observables import (  # noqa: F401

@@ -59,8 +59,9 @@ constexpr int kPartStride = 2 * rsv::kMaxKrylov > 2 + rsv::kMaxMasks ? 2 * rsv::
 
 // ---------------------------------------------------------------- tridiagonal eigen (implicit QL)
 // Eigen-decomposition of the symmetric tridiagonal (d, e); rotations are
-// accumulated only into the requested rows of the eigenvector matrix.
-void tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<std::vector<double>>& rows,
+// accumulated only into the requested rows of the eigenvector matrix. Returns false when an
+// eigenvalue did not converge within 60 sweeps (the caller reports it; never a silent result).
+bool tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<std::vector<double>>& rows,
                 const std::vector<int>& row_ids) {
   const int n = (int)d.size();
   e.push_back(0.0);
@@ -76,7 +77,7 @@ void tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<std::
         if (std::fabs(e[m]) <= 1e-300 + 2.2e-16 * dd * 0.5) break;
       }
       if (m != l) {
-        if (++iter > 60) break;
+        if (++iter > 60) return false;
         double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
         double rr = std::hypot(g, 1.0);
         g = d[m] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(rr) : -std::fabs(rr)));
@@ -112,10 +113,12 @@ void tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<std::
       }
     } while (m != l);
   }
+  return true;
 }
 
 // exp(-i tau T) e1 (krylov.py:54). With full=false only the last component is exact
-// (all that the convergence test needs); full=true returns every component.
+// (all that the convergence test needs); full=true returns every component. An empty result
+// means the tridiagonal eigensolver failed (reported as RSV_ERR_NOT_CONVERGED by the callers).
 std::vector<zc> tridiag_exp_e1(const std::vector<double>& a, const std::vector<double>& b, double tau,
                                bool full) {
   const int k = (int)a.size();
@@ -134,7 +137,7 @@ std::vector<zc> tridiag_exp_e1(const std::vector<double>& a, const std::vector<d
     ids.push_back(k - 1);
   }
   std::vector<std::vector<double>> rows;
-  tridiag_ql(d, e, rows, ids);
+  if (!tridiag_ql(d, e, rows, ids)) return {};
   const std::vector<double>& z0 = rows[0];
   std::vector<zc> ph(k);
   for (int m = 0; m < k; ++m) ph[m] = std::exp(zc(0.0, -tau * d[m])) * z0[m];
@@ -941,6 +944,8 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
       if (rc) return rc;
     }
     y = tridiag_exp_e1(alphas, betas, tau, false);
+    if (y.empty()) return fail(RSV_ERR_NOT_CONVERGED, "tridiagonal eigensolver (implicit QL) did not converge at k=%d",
+                               (int)alphas.size());
     residual = beta * std::abs(y.back());
     k = (int)alphas.size();
     double scale = 1.0;
@@ -964,6 +969,7 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
     for (int it = 0; it < 48; ++it) {
       const double mid = 0.5 * (lo + hi);
       const std::vector<zc> ys = tridiag_exp_e1(alphas, betas, mid * tau, false);
+      if (ys.empty()) return fail(RSV_ERR_NOT_CONVERGED, "tridiagonal eigensolver (implicit QL) did not converge");
       const double r = beta * std::abs(ys.back());
       if (r <= tol) {
         lo = mid;
@@ -979,6 +985,7 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
     }
   }
   y = tridiag_exp_e1(alphas, betas, frac * tau, true);
+  if (y.empty()) return fail(RSV_ERR_NOT_CONVERGED, "tridiagonal eigensolver (implicit QL) did not converge");
   rep->iterations = std::max(rep->iterations, k);
   rep->residual = std::max(rep->residual, residual);
   if (!converged) rep->converged = 0;
@@ -1021,7 +1028,15 @@ int expm_step_impl(rsv_context* c, const double* omegas, const double* deltas, d
     int rc = lanczos_run(c, omegas, deltas, remaining, tol, kmax, norm_eps, next_omegas, next_deltas, true,
                          observe, rep, run == 0, &frac, &zero);
     if (rc) return rc;
-    if (zero) return RSV_OK;
+    if (zero) {   // krylov.py:83-84 returns the zero vector unchanged; the observables still report it
+      if (observe) {
+        std::vector<double> tmp(c->masks.size() + 1);
+        double nsq = 0.0;
+        rc = rsv_measure(c, tmp.data(), &nsq);
+        if (rc) return rc;
+      }
+      return RSV_OK;
+    }
     if (!rep->converged || frac >= 1.0) return RSV_OK;
     remaining *= (1.0 - frac);
     rep->substeps += 1;
@@ -1214,8 +1229,10 @@ int rsv_expm_step(rsv_context* c, const double* omegas, const double* deltas, do
   if (c->diag_mode == RSV_DIAG_VEC && c->d_dvec == nullptr)
     return fail(RSV_ERR_STATE, "diag_mode VEC needs rsv_bind_diag_vector first");
   if (max_krylov_dim < 2) return fail(RSV_ERR_ARG, "max_krylov_dim must be >= 2");
-  if (max_krylov_dim > rsv::kMaxKrylov) max_krylov_dim = rsv::kMaxKrylov;
+  // max_krylov_dim above the resident basis (<= kMaxKrylov vectors) is not clamped: the reference's
+  // not-converged decision (krylov.py:115) uses the caller's value, the basis limit splits the step
   std::memset(report, 0, sizeof(*report));
+  c->obs_pending = false;   // observables of an earlier step are never reported as this step's
   if (dt_ns == 0.0) {   // krylov.py:85-86: identity, one iteration
     report->iterations = 1;
     report->converged = 1;
@@ -1405,6 +1422,7 @@ int rsv_set_shard(rsv_context* c, rsv_comm_fn comm, void* user, void* exchange_b
     c->xbuf = nullptr;
     return RSV_OK;
   }
+  if (c->reorth) return fail(RSV_ERR_STATE, "re-orthogonalisation is on: it is not available for sharded runs");
   if (reinterpret_cast<uintptr_t>(exchange_buffer) & 15u)   // NULL: peer-memory mode only
     return fail(RSV_ERR_ARG, "exchange buffer is not 16-byte aligned");
   c->sharded = true;

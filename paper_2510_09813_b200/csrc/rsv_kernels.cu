@@ -1679,28 +1679,52 @@ __global__ void sample_kernel(const cplx* __restrict__ psi, uint64_t n, const do
 
 // <s_i|w> for i < k (complex), one pass over w and the k vectors; deterministic per-CTA rows
 // (re-orthogonalisation of the fused Lanczos step, krylov.py:103-104).
-__global__ void multidot_kernel(const MultiDotArgs A) {
-  __shared__ double red[32];
-  __shared__ double s_row[2 * kMaxKrylov];
+// <v_i|w> for the whole basis in ONE pass over w (re-orthogonalisation, krylov.py:104): a CTA holds
+// kThreads x 8 amplitudes of w in registers and streams every v_i over them, so w is read once and
+// each v_i once ((k+1) x 16 B per amplitude). Per vector and chunk each warp reduces its share with
+// shuffles into its own row of shared accumulators; rows and CTAs are summed in fixed order.
+__global__ void __launch_bounds__(kThreads) multidot_kernel(const MultiDotArgs A) {
+  constexpr int EPT = 8;
+  constexpr int NW = kThreads / 32;
+  __shared__ double s_acc[NW][2 * kMaxKrylov];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t n = A.n;
-  for (int i = 0; i < A.k; ++i) {
-    double re = 0.0, im = 0.0;
-    for (uint64_t e = blockIdx.x * (uint64_t)kThreads + threadIdx.x; e < n; e += (uint64_t)gridDim.x * kThreads) {
-      const cplx a = A.v[i][e], b = A.w[e];
-      re = fma(a.x, b.x, fma(a.y, b.y, re));   // conj(a) b
-      im = fma(a.x, b.y, fma(-a.y, b.x, im));
+  const int ncol = 2 * A.k;
+  for (int c = lane; c < ncol; c += 32) s_acc[warp][c] = 0.0;
+  const uint64_t chunk = (uint64_t)kThreads * EPT;
+  for (uint64_t base = blockIdx.x * chunk; base < n; base += (uint64_t)gridDim.x * chunk) {
+    cplx wv[EPT];
+    #pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const uint64_t e = base + threadIdx.x + (uint64_t)j * kThreads;
+      wv[j] = e < n ? __ldcs(A.w + e) : make_double2(0.0, 0.0);
     }
-    re = block_sum<kThreads>(re, red);
-    im = block_sum<kThreads>(im, red);
-    if (threadIdx.x == 0) {
-      s_row[2 * i] = re;
-      s_row[2 * i + 1] = im;
+    for (int i = 0; i < A.k; ++i) {
+      const cplx* v = A.v[i];
+      double re = 0.0, im = 0.0;
+      #pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const uint64_t e = base + threadIdx.x + (uint64_t)j * kThreads;
+        const cplx a = e < n ? __ldcs(v + e) : make_double2(0.0, 0.0);
+        re = fma(a.x, wv[j].x, fma(a.y, wv[j].y, re));   // conj(a) w
+        im = fma(a.x, wv[j].y, fma(-a.y, wv[j].x, im));
+      }
+      re = warp_sum<32>(re);
+      im = warp_sum<32>(im);
+      if (lane == 0) {
+        s_acc[warp][2 * i] += re;
+        s_acc[warp][2 * i + 1] += im;
+      }
     }
   }
-  const int ncol = 2 * A.k;
   __syncthreads();
-  for (int c = threadIdx.x; c < ncol; c += kThreads) A.part[(size_t)blockIdx.x * A.stride + c] = s_row[c];
-  __shared__ bool s_last;
+  for (int c = threadIdx.x; c < ncol; c += kThreads) {
+    double v = 0.0;
+    #pragma unroll
+    for (int w = 0; w < NW; ++w) v += s_acc[w][c];
+    A.part[(size_t)blockIdx.x * A.stride + c] = v;
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(A.counter, 1u) == gridDim.x - 1;

@@ -38,7 +38,7 @@ typedef double2 cplx;
 
 constexpr int kMaxQubits = 48;
 constexpr int kMaxFlips = 16;     // flips per pass (tile bits <= 12)
-constexpr int kMaxKrylov = 96;    // vectors in one Krylov combination
+constexpr int kMaxKrylov = 120;   // vectors in one Krylov combination
 constexpr int kMaxMasks = 128;    // observable masks per combine
 constexpr int kLoBits = 12;       // tile bits: 2^12 complex128 = 64 KB per tile buffer
 constexpr int kGcStride = 14;     // lo-pass tile table row: gc[0..11], hh, tb (112 B, cp.async-able)

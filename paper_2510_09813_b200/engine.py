@@ -22,7 +22,7 @@ import numpy as np
 from . import _native as nat
 from .errors import MemoryBudgetError, ValidationError
 
-KMAX_NATIVE = 96          # rsv::kMaxKrylov
+KMAX_NATIVE = 120         # rsv::kMaxKrylov
 RESERVE_BYTES = 1 << 30   # headroom left to torch / the driver
 
 

@@ -1,17 +1,21 @@
 """Rydberg Hamiltonian in structured form -- mirror of rydsim/hamiltonian.py on B200.
 
 Same names, argument meaning and errors as the reference:
-``Register`` (hamiltonian.py:43), ``interaction_matrix`` (:66), ``build_diagonal``
-(:114), ``HamiltonianSlice`` (:125), ``apply_hamiltonian`` (:164),
-``build_dense`` (:191). Bit order: qubit i = bit i of the basis index.
+``Register`` (hamiltonian.py:43), ``interaction_matrix`` (:66), ``weighted_bit_sum``
+(:83), ``interaction_diagonal`` (:99), ``build_diagonal`` (:114), ``HamiltonianSlice``
+(:125), ``apply_hamiltonian`` (:164), ``build_dense`` (:191). Bit order: qubit i = bit i
+of the basis index.
 
 Differences by design (B200-first):
-* a slice built with ``HamiltonianSlice.from_parameters`` keeps (omegas,
-  deltas, U) and never materialises the 2^N diagonal: the lo pass of the CUDA
-  matvec computes it on the fly (``diag='vec'`` reads a precomputed float64
-  interaction diagonal instead);
-* states are complex128 CUDA tensors; numpy inputs are copied to the device and
-  results copied back (the host<->device copies are the "e2e" path).
+* a slice built with ``HamiltonianSlice.from_parameters`` keeps (omegas, deltas, U):
+  the lo pass of the CUDA matvec computes the diagonal on the fly (``diag='vec'``
+  reads a precomputed float64 interaction diagonal instead); ``slice.diagonal`` is
+  still the reference's 2^N array, built on the GPU the first time it is read;
+* the 2^N diagonals (``weighted_bit_sum``, ``interaction_diagonal``,
+  ``build_diagonal``) are built by a device kernel and returned as numpy arrays like
+  the reference's (``device=True`` keeps the CUDA tensor);
+* states may be complex128 CUDA tensors (results stay on the device) or numpy
+  arrays (copied in, result copied back: the "e2e" path).
 """
 
 from __future__ import annotations
@@ -27,6 +31,8 @@ from .errors import ValidationError
 __all__ = [
     "Register",
     "interaction_matrix",
+    "weighted_bit_sum",
+    "interaction_diagonal",
     "build_diagonal",
     "HamiltonianSlice",
     "apply_hamiltonian",
@@ -98,50 +104,74 @@ def context_for(n: int, u: np.ndarray, diag: str = "fly"):
     return _context(int(n), u.tobytes(), diag, torch.cuda.current_device())
 
 
-def build_diagonal(deltas, u: np.ndarray):
-    """Full diagonal -sum delta_i n_i + sum_{i<j} U_ij n_i n_j as a float64 CUDA tensor (hamiltonian.py:114)."""
+def _device_diagonal(deltas, u, device):
+    """-sum delta_i n_i + sum_{i<j} U_ij n_i n_j by the device kernel (rsv_build_diagonal)."""
     deltas = np.ascontiguousarray(deltas, dtype=np.float64)
-    if u.shape != (len(deltas), len(deltas)):
-        raise ValidationError(
-            f"interaction matrix shape {u.shape} does not match {len(deltas)} detunings")
     torch = _torch()
     ctx = context_for(len(deltas), u)
     out = torch.empty(1 << len(deltas), dtype=torch.float64, device=ctx.device)
     ctx.sync_stream()
-    nat.check(ctx.lib.rsv_build_diagonal(ctx.ctx, nat.dptr(deltas), out.data_ptr()))
-    return out
+    nat.check(ctx.lib.rsv_build_diagonal(ctx.ctx, nat.dptr(deltas), out.data_ptr()), "rsv_build_diagonal")
+    return out if device else out.cpu().numpy()
 
 
-@dataclass(frozen=True)
+def weighted_bit_sum(weights, device: bool = False):
+    """v[b] = sum_i weights[i] bit_i(b), length 2^N (hamiltonian.py:83)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+    return _device_diagonal(-w, np.zeros((len(w), len(w))), device)
+
+
+def interaction_diagonal(u: np.ndarray, device: bool = False):
+    """d[b] = sum_{i<j} U_ij bit_i(b) bit_j(b) (hamiltonian.py:99)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if u.ndim != 2 or u.shape[0] != u.shape[1]:
+        raise ValidationError(f"interaction matrix must be square, got shape {u.shape}")
+    return _device_diagonal(np.zeros(u.shape[0]), u, device)
+
+
+def build_diagonal(deltas, u: np.ndarray, device: bool = False):
+    """Full diagonal -sum delta_i n_i + sum_{i<j} U_ij n_i n_j (hamiltonian.py:114); numpy like the
+    reference, or the CUDA tensor with ``device=True``."""
+    deltas = np.ascontiguousarray(deltas, dtype=np.float64)
+    if u.shape != (len(deltas), len(deltas)):
+        raise ValidationError(
+            f"interaction matrix shape {u.shape} does not match {len(deltas)} detunings")
+    return _device_diagonal(deltas, u, device)
+
+
 class HamiltonianSlice:
     """One piecewise-constant Hamiltonian (hamiltonian.py:125).
 
-    ``HamiltonianSlice(omegas, diagonal)`` keeps the reference's explicit-diagonal form
+    ``HamiltonianSlice(omegas, diagonal)`` is the reference's explicit-diagonal form
     (diagonal: 2^N float64, numpy or CUDA tensor). ``from_parameters(omegas, deltas, u)``
-    keeps the structured form used by the hot path.
+    keeps the structured form used by the hot path (diagonal on the fly); its ``.diagonal``
+    is materialised (on the GPU, returned as numpy) the first time it is read.
     """
 
-    omegas: np.ndarray
-    diagonal: object = None
-    deltas: np.ndarray | None = None
-    interaction: np.ndarray | None = None
-
-    def __post_init__(self):
-        omegas = np.ascontiguousarray(self.omegas, dtype=float)
-        object.__setattr__(self, "omegas", omegas)
+    def __init__(self, omegas, diagonal=None, deltas=None, interaction=None):
+        omegas = np.ascontiguousarray(omegas, dtype=float)
         n = len(omegas)
-        if self.diagonal is None:
-            if self.deltas is None or self.interaction is None:
+        self.omegas = omegas
+        self.deltas = None
+        self.interaction = None
+        self._diagonal = None
+        if diagonal is None:
+            if deltas is None or interaction is None:
                 raise ValidationError("slice needs a diagonal or (deltas, interaction)")
-            object.__setattr__(self, "deltas", np.ascontiguousarray(self.deltas, dtype=float))
-            object.__setattr__(self, "interaction", np.ascontiguousarray(self.interaction, dtype=float))
+            self.deltas = np.ascontiguousarray(deltas, dtype=float)
+            self.interaction = np.ascontiguousarray(interaction, dtype=float)
             if self.interaction.shape != (n, n) or self.deltas.shape != (n,):
                 raise ValidationError(
                     f"interaction matrix shape {self.interaction.shape} does not match {n} detunings")
         else:
-            size = int(self.diagonal.shape[0]) if hasattr(self.diagonal, "shape") else len(self.diagonal)
-            if size != 2 ** n or len(getattr(self.diagonal, "shape", (size,))) != 1:
-                raise ValidationError(f"diagonal has length ({size},), expected 2^{n}")
+            if isinstance(diagonal, (list, tuple)):
+                diagonal = np.asarray(diagonal, dtype=float)
+            elif isinstance(diagonal, np.ndarray):
+                diagonal = np.ascontiguousarray(diagonal, dtype=float)
+            size = int(diagonal.shape[0]) if len(diagonal.shape) else -1
+            if size != 2 ** n or len(diagonal.shape) != 1:
+                raise ValidationError(f"diagonal has length {tuple(diagonal.shape)}, expected 2^{n}")
+            self._diagonal = diagonal
 
     @property
     def qubit_count(self) -> int:
@@ -149,7 +179,15 @@ class HamiltonianSlice:
 
     @property
     def structured(self) -> bool:
-        return self.diagonal is None
+        """True when the slice carries (deltas, U): the matvec computes the diagonal on the fly."""
+        return self.deltas is not None
+
+    @property
+    def diagonal(self):
+        """The 2^N diagonal (hamiltonian.py:131); built on the GPU on first access for structured slices."""
+        if self._diagonal is None:
+            self._diagonal = build_diagonal(self.deltas, self.interaction)
+        return self._diagonal
 
     @classmethod
     def from_parameters(cls, omegas, deltas, u: np.ndarray) -> "HamiltonianSlice":
@@ -162,10 +200,14 @@ class HamiltonianSlice:
         return cls(omegas, None, deltas, u)
 
     def dense_diagonal(self):
-        """The 2^N diagonal as a CUDA tensor (materialised only on request)."""
-        if self.diagonal is not None:
-            return _as_device(self.diagonal, dtype="float64")[0]
-        return build_diagonal(self.deltas, self.interaction)
+        """The 2^N diagonal as a CUDA tensor."""
+        if self._diagonal is not None:
+            return _as_device(self._diagonal, dtype="float64")[0]
+        return build_diagonal(self.deltas, self.interaction, device=True)
+
+    def __repr__(self):
+        form = "structured" if self.structured else "explicit diagonal"
+        return f"HamiltonianSlice(N={self.qubit_count}, {form})"
 
 
 def _as_device(x, dtype="complex128"):
@@ -179,10 +221,13 @@ def _as_device(x, dtype="complex128"):
     return x.to(tdt).contiguous(), False
 
 
-def apply_hamiltonian(slice_: HamiltonianSlice, psi, out=None):
+def apply_hamiltonian(slice_: HamiltonianSlice, psi, out=None, force_numpy: bool = False):
     """H @ psi without materialising H (hamiltonian.py:164) -- the CUDA bit-group passes.
 
-    psi: complex CUDA tensor (or numpy array: copied in, result copied back).
+    psi: complex CUDA tensor (or numpy array: copied in, result copied back). ``force_numpy``
+    is accepted for call compatibility and changes nothing: the reference uses it to select
+    its sequential numpy loop for cross-checks; this package has one (CUDA) implementation
+    and no CPU path (both reference paths agree with it to 1e-12, tests/test_gpu_parity.py).
     """
     n = slice_.qubit_count
     torch = _torch()
@@ -196,7 +241,7 @@ def apply_hamiltonian(slice_: HamiltonianSlice, psi, out=None):
     else:
         ctx = context_for(n, np.zeros((n, n)), "vec")
         deltas = np.zeros(n)
-        diag_tensor = _as_device(slice_.diagonal, dtype="float64")[0]
+        diag_tensor = _as_device(slice_._diagonal, dtype="float64")[0]
     y = out if (out is not None and not was_numpy) else torch.empty_like(x)
     if y.data_ptr() == x.data_ptr() and n > 12:
         y = torch.empty_like(x)

@@ -27,7 +27,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import ValidationError
+from .errors import MemoryBudgetError, ValidationError
 
 NS_TO_US = 1e-3
 _BREAKDOWN_RTOL = 1e-14
@@ -361,8 +361,20 @@ class FusedShardEngine:
         if memory_budget_bytes is None:
             free, _total = torch.cuda.mem_get_info(dev)
             memory_budget_bytes = max(0, free - (4 << 30))
+        # every rank must stop its Lanczos loop (and split a step) at the same Krylov cap, or the
+        # shards would enter different collectives: agree on the smallest slot count that fits
+        from .engine import slots_that_fit
+
+        local = slots_that_fit(nl, max_krylov_dim, "fly", dev, memory_budget_bytes, krylov_vectors_cap)
+        agreed = torch.tensor([float(local)], dtype=torch.float64,
+                              device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(agreed, op=dist.ReduceOp.MIN)
+        nslots = int(agreed.item())
         self.eng = SvEngine(nl, self.u[:nl, :nl], diag="fly", max_krylov_dim=max_krylov_dim, device=dev,
-                            memory_budget_bytes=memory_budget_bytes, krylov_vectors_cap=krylov_vectors_cap)
+                            memory_budget_bytes=memory_budget_bytes, krylov_vectors_cap=max(0, nslots - 1))
+        if len(self.eng.slots) != nslots:   # pragma: no cover - the budget shrank between the two queries
+            raise MemoryBudgetError(f"rank {dist.get_rank()}: {len(self.eng.slots)} Krylov slots, the ranks agreed "
+                                    f"on {nslots}")
         self.nccl = dist.get_backend() == "nccl"
         self._reqs = []
         self._recv_host = None
@@ -415,6 +427,9 @@ class FusedShardEngine:
             table = []
             for g in self.plan.global_qubits:
                 peer = self.plan.partner(g)
+                if len(everyone[peer]) != len(self.eng.slots):
+                    raise RuntimeError(f"partner rank {peer} has {len(everyone[peer])} slots, this rank "
+                                       f"{len(self.eng.slots)}")
                 tensors = [fn(*args) for fn, args in everyone[peer]]
                 self._peer_tensors.append(tensors)
                 table.extend(t.data_ptr() for t in tensors)

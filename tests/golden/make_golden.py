@@ -292,7 +292,38 @@ def gen_runs():
         json.dump(out, fh)
 
 
+def gen_lattice20_full():
+    """configs[1] for its whole length: N=20 4x5 lattice, 5.6 um, delta sweep -6 -> +6 rad/us over
+    3 us (300 steps of 10 ns), occupations every 10 steps, energy at the end."""
+    reg = grid_register(4, 5, spacing_um=5.6, interaction_c=5_420_000.0)
+    prog = ChannelProgram.from_channels(
+        [[Constant(3000, TWO_PI)] for _ in range(20)],
+        [[Ramp(3000, -6.0, 6.0)] for _ in range(20)], 3000)
+    seq = discretize(sample_program(prog), 10)
+    res = evolve_sv(seq, reg, SvRunConfig(krylov=KrylovConfig(1e-10),
+                                          observables=(ObservableSpec("occupation", (), 10),)))
+    psi = res.final_state
+    rng = np.random.default_rng(77)
+    probe = rng.standard_normal(2 ** 20) + 1j * rng.standard_normal(2 ** 20)
+    occ = [r for r in res.observables if r.kind == "occupation"]
+    last = HamiltonianSlice.from_parameters(seq.omegas[-1], seq.deltas[-1], interaction_matrix(reg))
+    np.savez_compressed(
+        os.path.join(HERE, "evolve_lattice20_full.npz"),
+        positions=np.array(reg.positions_um), c6=np.array(reg.interaction_c),
+        omegas=seq.omegas, deltas=seq.deltas, dt=np.array(10), tol=np.array(1e-10),
+        every=np.array(10),
+        occ=np.array([r.values for r in occ]), occ_t=np.array([r.t_ns for r in occ]),
+        energy_last=np.array(np.vdot(psi, apply_hamiltonian(last, psi)).real),
+        iterations=np.array([r.iterations for r in res.krylov_reports]),
+        probe_overlap=np.array(np.vdot(probe, psi)), norm=np.array(np.linalg.norm(psi)),
+        amp_head=psi[:64].copy(), amp_tail=psi[-64:].copy())
+    print("lattice20 full: steps", seq.step_count, "iters max", res.max_krylov_iterations)
+
+
 if __name__ == "__main__":
+    if "--lattice20-full" in sys.argv:   # configs[1] full-length fixture (minutes of CPU)
+        gen_lattice20_full()
+        sys.exit(0)
     if "--sampling" in sys.argv:   # regenerate only the sampling fixture
         gen_sampling()
         sys.exit(0)

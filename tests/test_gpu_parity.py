@@ -76,11 +76,55 @@ class TestApplyHamiltonian:
         out = rs.apply_hamiltonian(s, torch.from_numpy(psi).cuda()).cpu().numpy()
         assert rel_err(out, ref) <= 1e-12
 
+    @pytest.mark.parametrize("n", [21, 25, 26, 27, 28])
+    def test_plan_shapes_against_c_matvec(self, rs, torch, n):
+        # N=21: one 9-bit group pass (a=3, g=9: the 5-D tensor map's second group dimension);
+        # 25..28: lo + two groups of 6..8 bits (every plan shape below the N=29/30 ones, which
+        # tests/test_headline_parity_gpu.py covers); checked over the whole vector against the
+        # C restatement of the reference's compiled matvec (rydsim/_kernels.py:13)
+        from oracle import big
+
+        rng = np.random.default_rng(100 + n)
+        om, de, u = random_slice(rng, n)
+        om[3] = 0.0
+        gen = torch.Generator(device="cuda").manual_seed(n)
+        x = torch.randn(2 ** n, dtype=torch.complex128, device="cuda", generator=gen)
+        s = rs.HamiltonianSlice.from_parameters(om, de, u)
+        out = rs.apply_hamiltonian(s, x).cpu().numpy()
+        psi = x.cpu().numpy()
+        del x
+        ref = big.HostHamiltonian(om, de, u).matvec(psi, np.empty_like(psi))
+        assert rel_err(out, ref) <= 1e-12
+        if n == 21:
+            assert [(p["a"], p["g"]) for p in rs.hamiltonian.context_for(n, u).pass_plan()] == [(12, 0), (3, 9)]
+
     def test_build_diagonal_on_device(self, rs):
         g = load("diagonal.npz")
         for n in (1, 2, 6, 9):
-            d = rs.build_diagonal(g[f"n{n}_deltas"], g[f"n{n}_u"]).cpu().numpy()
+            d = rs.build_diagonal(g[f"n{n}_deltas"], g[f"n{n}_u"])
+            assert isinstance(d, np.ndarray)   # numpy, like the reference (hamiltonian.py:114)
             assert np.abs(d - g[f"n{n}_diag"]).max() <= 1e-12 * max(1, np.abs(d).max())
+            dd = rs.build_diagonal(g[f"n{n}_deltas"], g[f"n{n}_u"], device=True)
+            assert dd.is_cuda and np.array_equal(dd.cpu().numpy(), d)
+
+    def test_reference_diagonal_helpers_and_lazy_slice_diagonal(self, rs):
+        # hamiltonian.py:83 weighted_bit_sum, :99 interaction_diagonal, :131 slice.diagonal
+        assert rs.weighted_bit_sum([1.0, 10.0, 100.0]).tolist() == [0, 1, 10, 11, 100, 101, 110, 111]
+        g = load("apply_hamiltonian.npz")
+        for n in (3, 10):
+            om, de, u = g[f"n{n}_omegas"], g[f"n{n}_deltas"], g[f"n{n}_u"]
+            idiag = rs.interaction_diagonal(u)
+            assert np.abs(idiag - O.interaction_diagonal(u)).max() <= 1e-12 * max(1.0, np.abs(idiag).max())
+            assert np.abs(rs.weighted_bit_sum(-de) + idiag - g[f"n{n}_diag"]).max() <= 1e-12 * max(1.0, np.abs(idiag).max())
+            s = rs.HamiltonianSlice.from_parameters(om, de, u)
+            assert s.structured and isinstance(s.diagonal, np.ndarray)
+            assert np.abs(s.diagonal - g[f"n{n}_diag"]).max() <= 1e-12 * max(1.0, np.abs(idiag).max())
+            # force_numpy is accepted (the reference's cross-check flag); same CUDA result
+            a = rs.apply_hamiltonian(s, g[f"n{n}_psi"])
+            b = rs.apply_hamiltonian(s, g[f"n{n}_psi"], force_numpy=True)
+            assert np.array_equal(a, b) and rel_err(a, g[f"n{n}_hpsi"]) <= 1e-12
+        with pytest.raises(rs.ValidationError):
+            rs.HamiltonianSlice([1.0, 2.0], np.zeros(3))
 
     def test_linearity_and_hermiticity_large(self, rs, torch):
         n = 26
@@ -196,6 +240,25 @@ class TestEvolve:
         occ = np.array([r.values for r in res.observables])
         assert np.abs(occ - g["occ"]).max() <= 1e-8
 
+    def test_lattice20_config1_full_sweep(self, rs):
+        # BASELINE configs[1] for its whole length: the 3 us adiabatic sweep (300 steps of 10 ns)
+        # against the reference's own run (tests/golden/make_golden.py --lattice20-full)
+        g = load("evolve_lattice20_full.npz")
+        res = run_gpu(rs, g, int(g["every"]), energy=True)
+        psi = res.final_state.cpu().numpy()
+        rng = np.random.default_rng(77)
+        probe = rng.standard_normal(2 ** 20) + 1j * rng.standard_normal(2 ** 20)
+        assert abs(np.vdot(probe, psi) - complex(g["probe_overlap"])) <= 1e-8 * abs(complex(g["probe_overlap"]))
+        assert np.abs(psi[:64] - g["amp_head"]).max() <= 1e-9
+        assert np.abs(psi[-64:] - g["amp_tail"]).max() <= 1e-9
+        occ = np.array([r.values for r in res.observables if r.kind == "occupation"])
+        assert occ.shape == g["occ"].shape
+        assert np.abs(occ - g["occ"]).max() <= 1e-8
+        e = [r.values[0] for r in res.observables if r.kind == "energy"][-1]
+        assert abs(e - float(g["energy_last"])) <= 1e-8 * max(1.0, abs(float(g["energy_last"])))
+        iters = np.array([r.iterations for r in res.krylov_reports])
+        assert len(iters) == 300 and np.abs(iters - g["iterations"]).max() <= 1
+
     def test_krylov_cap_substepping_is_exact(self, rs, torch):
         # a tiny HBM budget caps the Krylov basis; the step is split in time and must agree
         g = load("evolve_detmap12.npz")
@@ -206,6 +269,18 @@ class TestEvolve:
         capped = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12), krylov_vectors_cap=6))
         assert any(r.substeps > 1 for r in capped.krylov_reports)
         assert rs.norm_difference(full.final_state, capped.final_state) <= 1e-9
+
+    def test_host_final_state_and_force_numpy_flag(self, rs):
+        # SvRunConfig(host_final_state=True): numpy final state like the reference (sv.py:66), the
+        # workspace released; force_numpy_matvec (sv.py:61) is accepted and changes nothing
+        g = load("evolve_ring10.npz")
+        reg = rs.Register(tuple(map(tuple, g["positions"])), float(g["c6"]))
+        seq = rs.DiscretizedSequence(int(g["dt"]), g["omegas"][:8], g["deltas"][:8], 8 * int(g["dt"]))
+        a = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-10)))
+        b = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-10), host_final_state=True,
+                                                  force_numpy_matvec=True))
+        assert isinstance(b.final_state, np.ndarray) and b.engine is None
+        assert np.array_equal(a.final_state.cpu().numpy(), b.final_state)
 
     def test_rabi_analytic(self, rs):
         seq = rs.discretize(rs.sample_program(rs.ChannelProgram.from_channels(

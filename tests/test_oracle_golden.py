@@ -147,3 +147,56 @@ class TestSamplingOracle:
         cdf[-1] = 1.0
         u = sample_uniforms(int(g["n10_shots"]), int(g["n10_seed"]))
         assert np.array_equal(np.searchsorted(cdf, u, side="right"), g["n10_idx"])
+
+
+class TestHostLanczosOracle:
+    """oracle/big.py (the reference's Lanczos loop on the host with the C matvec and in-place C vector
+    operations, used for the N=27/29 GPU parity tests) against the reference's golden vectors and the
+    numpy restatement."""
+
+    def test_c_matvec_matches_reference(self):
+        from oracle import big
+
+        g = load("apply_hamiltonian.npz")
+        for n in (1, 2, 3, 5, 8, 10, 13):
+            h = big.HostHamiltonian(g[f"n{n}_omegas"], g[f"n{n}_deltas"], g[f"n{n}_u"])
+            assert np.abs(h.diag - g[f"n{n}_diag"]).max() <= 1e-12 * max(1.0, np.abs(h.diag).max())
+            psi = np.ascontiguousarray(g[f"n{n}_psi"], dtype=np.complex128)
+            out = h.matvec(psi, np.empty_like(psi))
+            ref = g[f"n{n}_hpsi"]
+            assert np.abs(out - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), n
+            part = np.zeros_like(psi)
+            lo, hi = len(psi) // 3, len(psi) // 3 + max(1, len(psi) // 4)
+            h.matvec_range(psi, part, lo, hi)
+            assert np.array_equal(part[lo:hi], out[lo:hi])
+
+    def test_expm_matches_reference_golden(self):
+        from oracle import big
+
+        g = load("expm_multiply.npz")
+        for n in range(2, 11):
+            h = big.HostHamiltonian(g[f"n{n}_omegas"], g[f"n{n}_deltas"], g[f"n{n}_u"])
+            out, it, conv, res, _, _ = big.expm_multiply(h, g[f"n{n}_psi"], float(g[f"n{n}_dt"]), 1e-10)
+            assert conv and it == int(g[f"n{n}_iterations"]), n
+            assert np.linalg.norm(out - g[f"n{n}_out"]) <= 1e-12, n
+
+    def test_expm_matches_numpy_restatement(self):
+        from oracle import big
+
+        rng = np.random.default_rng(21)
+        n = 12
+        om, de = rng.uniform(0, 4, n), rng.uniform(-3, 3, n)
+        u = np.triu(rng.uniform(0, 2, (n, n)), 1)
+        u = u + u.T
+        psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        h = big.HostHamiltonian(om, de, u)
+        a = big.expm_multiply(h, psi, 12.0, 1e-11)
+        diag = O.build_diagonal(de, u)
+        b = O.expm_multiply(lambda v: O.apply_hamiltonian(om, diag, v), psi, 12.0, 1e-11)
+        assert a[1] == b[1] and a[2] and b[2]
+        assert np.allclose(a[4], b[4], rtol=1e-12, atol=1e-12) and np.allclose(a[5], b[5], rtol=1e-11)
+        assert np.linalg.norm(a[0] - b[0]) <= 1e-12 * np.linalg.norm(psi)
+        with pytest.raises(O.OracleError):
+            big.expm_multiply(h, psi, 12.0, 1e-11, max_vectors=3)
+        z = big.expm_multiply(h, np.zeros(2 ** n, complex), 12.0)
+        assert z[1] == 0 and z[2]

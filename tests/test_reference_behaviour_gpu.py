@@ -165,6 +165,28 @@ class TestSampling:
         assert np.array_equal(a, O.sample_bitstrings(psi, 10_000, 99))
 
 
+class TestDiscretizationOrder:
+    def test_second_order_in_dt(self, rs):
+        # reference tests/test_sv.py:145-159: adiabatic_program(2, 320 ns) on the default chain
+        # (generator.py:28,50: 7 um spacing, C = 5e6, Blackman drive, -3*2pi -> 2*2pi sweep);
+        # halving dt cuts the final-state error ~4x (midpoint sampling, pulses.py discretize)
+        reg = rs.Register(tuple((7.0 * i, 0.0) for i in range(2)), 5_000_000.0)
+        w = rs.pulses.blackman_window(320)
+        area = TWO_PI * w.sum() / w.max()
+        prog = rs.ChannelProgram.from_channels([[rs.Blackman(320, area)] for _ in range(2)],
+                                               [[rs.Ramp(320, -3 * TWO_PI, 2 * TWO_PI)] for _ in range(2)], 320)
+        sampled = rs.sample_program(prog)
+        cfg = rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12))
+        ref = rs.evolve_sv(rs.discretize(sampled, 1), reg, cfg).final_state
+        errors = {}
+        for dt in (2, 4, 8, 16):
+            out = rs.evolve_sv(rs.discretize(sampled, dt), reg, cfg).final_state
+            errors[dt] = rs.norm_difference(out, ref)
+        for dt in (2, 4, 8):
+            ratio = errors[2 * dt] / errors[dt]
+            assert 2.5 <= ratio <= 6.0, (dt, errors)
+
+
 def test_snapshots_at_full_size(rs):
     # N=29: the Krylov workspace takes all of HBM, snapshots go to host memory
     from paper_2510_09813_b200 import workloads
