@@ -219,6 +219,17 @@ def run_reference(args):
     t0 = time.time()
     steps = args.steps
     res = cpu_baseline(args.n, steps=steps, warmup=args.warmup, chunk_log2=max(0, args.n - 24))
+    # second leg: the reference's own kernel as the reference runs it (numba, serial), restated in
+    # oracle/numba_ref.py (identical outputs to rydsim/_kernels.py:13: profiles/r2_numba_reference.json)
+    numba_leg = None
+    if not args.no_numba:
+        try:
+            from oracle import numba_ref
+
+            numba_leg = numba_ref.time_sample(args.n, seconds=args.numba_seconds)
+            numba_leg.pop("elapsed_s", None)
+        except Exception as exc:  # pragma: no cover - numba missing on the host
+            numba_leg = {"value": None, "sample": f"unavailable: {exc}"}
     line = {
         "impl": "reference", "metric": BASELINE_METRIC, "value": res["value"], "unit": "H.psi/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
@@ -230,6 +241,7 @@ def run_reference(args):
         "cpu_baseline": {"value": res["value"], "unit": "H.psi/s", "cores": res["cores"], "kind": "port",
                          "sample": res["sample"]},
         "e2e": {"value": res["value"], "unit": "H.psi/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_numba": numba_leg,
         "wall_s": time.time() - t0,
     }
     print(json.dumps(line), flush=True)
@@ -304,9 +316,15 @@ def run_sharded(args, rank, world, local, pg):
         return eng.step(*seq.step(k), float(seq.dt_ns), cfg.tolerance, cfg.max_krylov_dim, next_params=nxt,
                         observe=True)
 
+    w0 = torch.cuda.Event(enable_timing=True)
+    w1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    w0.record(stream)
     for k in range(args.warmup):
         do_step(k)
+    w1.record(stream)
     torch.cuda.synchronize()
+    warm_ms = max_over_ranks(w0.elapsed_time(w1), pg)
     barrier(pg)
     eng.eng.set_profiling(True)
     sampler = ClockSampler(local)
@@ -364,6 +382,22 @@ def run_sharded(args, rank, world, local, pg):
                "path": "paper_2510_09813_b200.sharding.evolve_sv_sharded_fused(host shard in) + shard copied out"}
         del psi
         torch.cuda.empty_cache()
+    pulse_us = seq.dt_ns * seq.step_count / 1000.0
+    if total_steps == seq.step_count:
+        pulse_fields = {"s_per_us_pulse": (warm_ms + ms) / 1e3 / pulse_us,
+                        "pulse_measured_s": {"device": (warm_ms + ms) / 1e3, "steps": total_steps,
+                                             "e2e": (e2e["ms"] / 1e3) if e2e else None}}
+    else:
+        pulse_fields = {"s_per_us_pulse_extrapolated": ms / args.steps * seq.step_count / 1e3 / pulse_us,
+                        "pulse_measured_s": None}
+    # self-check of the multi-GPU run: the communicator saw every rank, one GPU per rank, and the mode
+    # (peer-memory P2P loads or exchange) that actually ran
+    devs = [None] * world
+    dist.all_gather_object(devs, (torch.cuda.current_device(), torch.cuda.get_device_properties(local).uuid.hex
+                                  if hasattr(torch.cuda.get_device_properties(local), "uuid") else str(local)))
+    mg_check = {"backend": dist.get_backend(), "world": dist.get_world_size(), "requested": args.gpus,
+                "distinct_gpus": len({d[1] for d in devs}), "peer_memory": bool(peer_mode),
+                "ok": dist.get_world_size() == args.gpus}
     if rank == 0:
         line = {
             "metric": BASELINE_METRIC, "value": value, "unit": "H.psi/s", "n_gpus": world, "steps": args.steps,
@@ -384,7 +418,8 @@ def run_sharded(args, rank, world, local, pg):
                 "l2": "inputs larger than L2 (shard = %.1f GB)" % (16 * 2 ** args.n / 1e9),
                 "krylov_vectors_resident": krylov_cap,
             },
-            "s_per_us_pulse": ms / args.steps * seq.step_count / 1e3 * (1000.0 / (seq.dt_ns * seq.step_count)),
+            **pulse_fields,
+            "multi_gpu_check": mg_check,
             "krylov": {"iterations_mean": k_avg, "iterations_max": max(iters) if iters else 0,
                        "matvecs": matvecs, "substeps": sum(r.substeps for r in reps)},
             "kernel_ms": {f: round(v["ms"], 3) for f, v in prof.items()},
@@ -394,7 +429,7 @@ def run_sharded(args, rank, world, local, pg):
             "gpu_launches": int(sum(v["launches"] for v in prof.values())),
             "clocks": clocks, "e2e": e2e, "cpu_baseline": None,
             "final_occupations": [round(float(x), 6) for x in occ],
-            "setup_s": round(time.time() - t_setup, 1),
+            "job_wall_s": round(time.time() - t_setup, 1),   # whole job incl. the e2e leg
         }
         print(json.dumps(line), flush=True)
     barrier(pg)
@@ -434,9 +469,15 @@ def run_ours(args):
         occ = eng.observables()   # device -> host read of the step's result
         return rep, occ
 
+    w0 = torch.cuda.Event(enable_timing=True)
+    w1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    w0.record(stream)
     for k in range(args.warmup):
         do_step(k)
+    w1.record(stream)
     torch.cuda.synchronize()
+    warm_ms = max_over_ranks(w0.elapsed_time(w1), pg)
     barrier(pg)
     eng.set_profiling(True)
     sampler = ClockSampler(local)
@@ -512,6 +553,27 @@ def run_ours(args):
         del res
         torch.cuda.empty_cache()
 
+    # s per 1 us pulse: measured only when warm-up + timed steps are the whole pulse (device time of
+    # all of its steps); otherwise an extrapolation from the timed steps, named as such
+    pulse_us = seq.dt_ns * seq.step_count / 1000.0
+    pulse_fields = {}
+    if total_steps == seq.step_count:
+        pulse_fields["s_per_us_pulse"] = (warm_ms + ms) / 1e3 / pulse_us
+        pulse_fields["pulse_measured_s"] = {"device": (warm_ms + ms) / 1e3,
+                                            "e2e": (e2e["ms"] / 1e3) if e2e else None,
+                                            "steps": total_steps}
+    else:
+        pulse_fields["s_per_us_pulse_extrapolated"] = ms_per_step * seq.step_count / 1e3 / pulse_us
+        pulse_fields["pulse_measured_s"] = None
+    # per-H.psi roofline: the irreducible 48 B/amp of a Lanczos iteration (read v_j, v_{j-1}, write w)
+    # over the device time of its passes (every family but the Krylov combination)
+    pass_total_ms = sum(v["ms"] for f, v in prof.items() if f != "combine")
+    irreducible = 48.0 * 2 ** n * matvecs
+    per_hpsi = {"irreducible_bytes_per_amp": 48, "iteration_ms": pass_total_ms / max(1, matvecs),
+                "achieved_gbs": irreducible / (pass_total_ms / 1e3) / 1e9 if pass_total_ms else None,
+                "frac": (irreducible / (pass_total_ms / 1e3) / 1e9 / hbm_peak) if pass_total_ms else None,
+                "passes_bytes_per_amp": 48 * (len(plan) if plan else 1)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -547,7 +609,7 @@ def run_ours(args):
                 "krylov_vectors_resident": krylov_cap,
             },
             "hbm_gbs_effective": eff_gbs,
-            "s_per_us_pulse": ms_per_step * seq.step_count / 1e3 * (1000.0 / (seq.dt_ns * seq.step_count)),
+            **pulse_fields,
             "krylov": {"iterations_mean": k_avg, "iterations_max": max(iters) if iters else 0,
                        "matvecs": matvecs, "substeps": substeps},
             "kernel_ms": pass_ms,
@@ -558,12 +620,13 @@ def run_ours(args):
                                             f"dram__bytes_write.sum of one {traffic_kernel} launch)"
                                             if traffic else None),
                          "alg_bytes_per_launch": alg, "avg_launch_ms": avg_launch_ms},
+            "per_hpsi": per_hpsi,
             "gpu_launches": kernel_launches,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "final_occupations": [round(x, 6) for x in final_occ],
-            "setup_s": round(time.time() - t_setup, 1),
+            "job_wall_s": round(time.time() - t_setup, 1),   # whole job incl. the e2e and CPU legs
         }
         print(json.dumps(line), flush=True)
     barrier(pg)
@@ -595,6 +658,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-numba", action="store_true", help="--impl reference: skip the serial numba leg")
+    ap.add_argument("--numba-seconds", type=float, default=10.0)
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("note: warm-up < 3 violates the timing rules", file=sys.stderr)
