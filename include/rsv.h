@@ -39,8 +39,11 @@ typedef struct {
   double residual;    /* final estimate |beta_k [exp(-i tau T_k)]_{k,1}| */
   double alpha0;      /* <v0|H|v0>: Rayleigh quotient of the input state (Energy observable) */
   double norm_in;     /* ||psi|| of the input state */
-  int substeps;       /* >1 when the Krylov basis hit the HBM cap and the step was split */
-  int matvecs;        /* H.psi products issued */
+  int substeps;       /* >0 when the step was split in time (basis beyond kMaxKrylov, or re-orthogonalisation
+                         with a basis beyond the resident slots) */
+  int matvecs;        /* H.psi products issued (including regenerated ones) */
+  int regenerated;    /* Lanczos vectors recomputed for the combination because the basis outgrew the
+                         resident slots (the recurrence continues in a ring of two slots) */
 } rsv_krylov_report;
 
 int rsv_version(void);
@@ -147,6 +150,17 @@ int rsv_set_shard_peers(rsv_context* ctx, int n_global, const void* const* ptrs,
 int rsv_enable_peer_access(const void* ptr);
 /* This shard's share of ||psi||^2 from the last Krylov combination / measurement. */
 int rsv_shard_local_norm_sq(rsv_context* ctx, double* out);
+
+/* Beyond the resident Krylov basis (nslots - 1 vectors) the fused step continues the recurrence in a
+ * ring of the last two slots and regenerates the overwritten vectors for the combination (default,
+ * on), or splits the step exactly in time (off; always the case with re-orthogonalisation). Either
+ * way the result meets the reference's tolerance; regeneration keeps the reference's Krylov
+ * dimension per step (krylov.py:96-117). */
+int rsv_set_tail_regeneration(rsv_context* ctx, int on);
+/* Launch Lanczos iteration j+1 before the host has tested iteration j for convergence (hides the host
+ * round trip on small registers; a speculative iteration after convergence is discarded):
+ * -1 auto (N <= 24, the default), 0 off, 1 on. Never in sharded or re-orthogonalised runs. */
+int rsv_set_speculation(rsv_context* ctx, int mode);
 
 /* Full re-orthogonalisation of every new Lanczos vector against the basis (the reference algorithm,
  * krylov.py:103-104; classical Gram-Schmidt, two extra passes over the basis per iteration). Off by

@@ -40,6 +40,7 @@ class KrylovReportC(ctypes.Structure):
         ("norm_in", ctypes.c_double),
         ("substeps", ctypes.c_int),
         ("matvecs", ctypes.c_int),
+        ("regenerated", ctypes.c_int),
     ]
 
 
@@ -88,6 +89,8 @@ SIGNATURES = {
     "rsv_pass_plan": (ctypes.c_int, [ctypes.c_void_p, c_int_p, ctypes.c_int]),
     "rsv_set_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]),
     "rsv_set_reorthogonalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rsv_set_tail_regeneration": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rsv_set_speculation": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_shard": (ctypes.c_int, [ctypes.c_void_p, COMM_FN, ctypes.c_void_p, ctypes.c_void_p]),
     "rsv_set_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                           c_double_p, c_int_p]),

@@ -54,6 +54,8 @@ int fail(int code, const char* fmt, ...) {
 constexpr double kNsToUs = 1e-3;          // krylov.py:21
 constexpr double kBreakdownRtol = 1e-14;  // krylov.py:25
 constexpr int kScratchJ = 127;            // alpha-partial slot used by plain H.psi
+constexpr int kRegenMax = rsv::kMaxKrylov; // Lanczos vectors of one run (device scalar arrays hold 128)
+constexpr int kSpeculateMaxQubits = 24;    // auto speculation: Lanczos iterations of <= ~0.5 ms
 constexpr int kPartStride = 2 * rsv::kMaxKrylov > 2 + rsv::kMaxMasks ? 2 * rsv::kMaxKrylov
                                                                       : 2 + rsv::kMaxMasks;   // widest partial row
 
@@ -237,6 +239,9 @@ struct rsv_context {
   // peer_slots[g][physical slot] for global qubit g (empty: exchange through the callback)
   std::vector<std::vector<const cplx*>> peer_slots;
   bool reorth = false;              // full re-orthogonalisation (krylov.py:103-104), opt-in
+  bool tail_regen = true;           // beyond the resident basis: ring + regeneration (else split in time)
+  int speculate = -1;               // launch iteration j+1 before testing j: -1 auto (N <= 24), 0 off, 1 on
+  cudaEvent_t iter_ev[2] = {nullptr, nullptr};
   double* d_dots = nullptr;         // <s_i|w> scratch (2 kMaxKrylov doubles)
   int plan_gm = -1;               // chunk group bits: -1 auto, 0 off, 3..9 forced (rsv_set_plan)
   long long plan_lag = -1;        // chunk scheduler lag in M tiles (-1 auto)
@@ -270,6 +275,15 @@ int kcap(const rsv_context* c) { return (int)c->logical.size() - 1; }
 cplx* slot(const rsv_context* c, int logical_index) {
   return reinterpret_cast<cplx*>(c->phys[c->logical[logical_index]]);
 }
+// Logical slot of Krylov vector s_i. Up to the cap K the basis is resident (s_i in slot i); beyond
+// it the recurrence continues in a ring of the last two slots (s_i for i > K overwrites s_{i-2}:
+// iteration j writes s_{j+1} where it read s_{j-1}, elementwise), and the overwritten basis
+// vectors are regenerated for the Krylov combination (lanczos_run, "tail regeneration").
+int kidx(const rsv_context* c, int i) {
+  const int K = kcap(c);
+  return i <= K ? i : (K - 1) + ((i - (K - 1)) & 1);
+}
+cplx* kvec(const rsv_context* c, int i) { return slot(c, kidx(c, i)); }
 
 // Pass plan: the lo pass (tile = bits [0, 12), carries the diagonal) and hi passes over groups
 // of <= 9 high bits (tile = 2^a contiguous x 2^g strided rows). Smaller groups sit at the top
@@ -481,16 +495,21 @@ void prof_end(rsv_context* c) {
   if (!c->prof) return;
   cudaEventRecord(c->ev_pool[c->ev_pending.back().first + 1], c->st);
 }
-void prof_collect(rsv_context* c) {   // call after a stream sync
+void prof_collect(rsv_context* c) {   // collects the kernels that have finished (speculation may leave some)
   if (!c->prof) return;
+  std::vector<std::pair<int, int>> left;
   for (auto& pe : c->ev_pending) {
+    if (cudaEventQuery(c->ev_pool[pe.first + 1]) != cudaSuccess) {
+      left.push_back(pe);
+      continue;
+    }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev_pool[pe.first], c->ev_pool[pe.first + 1]);
     c->prof_ms[pe.second] += ms;
     c->prof_n[pe.second] += 1;
   }
-  c->ev_pending.clear();
-  c->ev_next = 0;
+  c->ev_pending.swap(left);
+  if (c->ev_pending.empty()) c->ev_next = 0;
 }
 
 int family_of(size_t pass_index, size_t npass) {
@@ -551,14 +570,14 @@ int shard_before_last(rsv_context* c, int j, double sigma, bool started, bool p2
     int rc;
     if (!(first && started)) {
       CUDA_TRY(cudaStreamSynchronize(c->st));
-      rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[j], c->gpeer[g], nullptr, 0);
+      rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[kidx(c, j)], c->gpeer[g], nullptr, 0);
       if (rc) return rc;
     }
     first = false;
-    rc = comm_call(c, RSV_COMM_EXCHANGE_WAIT, c->logical[j], c->gpeer[g], nullptr, 0);
+    rc = comm_call(c, RSV_COMM_EXCHANGE_WAIT, c->logical[kidx(c, j)], c->gpeer[g], nullptr, 0);
     if (rc) return rc;
     const double cs = c->gcoef[g] * sigma;
-    CUDA_TRY(rsv::launch_global_flip(slot(c, j + 1), c->xbuf, slot(c, j), cs, nloc, c->d_part, c->d_counter,
+    CUDA_TRY(rsv::launch_global_flip(kvec(c, j + 1), c->xbuf, kvec(c, j), cs, nloc, c->d_part, c->d_counter,
                                      c->d_sc + rsv::SC_GF, c->st));
     double dot = 0.0;
     CUDA_TRY(cudaMemcpyAsync(&c->h_pin[rsv::SC_GF], c->d_sc + rsv::SC_GF, sizeof(double), cudaMemcpyDeviceToHost,
@@ -629,9 +648,11 @@ void classify_masks(rsv::CombineArgs& A) {
   }
 }
 
-// Krylov combination (also "prepare": k = 1, coefficient 1, in place).
+// Krylov combination (also "prepare": k = 1, coefficient 1, in place). vecs (optional): the vectors
+// to combine (default: s_0..s_{k-1} in their resident slots).
 int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, const double* q_omegas,
-                const double* q_deltas, int observe, double q_offset = 0.0) {
+                const double* q_deltas, int observe, double q_offset = 0.0,
+                const std::vector<const cplx*>* vecs = nullptr) {
   rsv::CombineArgs A{};
   const PassPlan& last = c->plan.back();
   A.sh = last.sh;
@@ -650,7 +671,7 @@ int run_combine(rsv_context* c, int k, const std::vector<zc>& coef, cplx* out, c
   if (k > rsv::kMaxKrylov) return fail(RSV_ERR_ARG, "Krylov combination of %d vectors exceeds %d", k, rsv::kMaxKrylov);
   A.k = k;
   for (int i = 0; i < k; ++i) {
-    A.v[i] = slot(c, i);
+    A.v[i] = vecs ? (*vecs)[i] : slot(c, i);
     A.coef[i] = make_double2(coef[i].real(), coef[i].imag());
   }
   A.out = out;
@@ -738,7 +759,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
       if (c->gcoef[g] == 0.0) continue;
       if (c->xbuf == nullptr) return fail(RSV_ERR_STATE, "exchange mode without an exchange buffer (rsv_set_shard)");
       CUDA_TRY(cudaStreamSynchronize(c->st));
-      int rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[j], c->gpeer[g], nullptr, 0);
+      int rc = comm_call(c, RSV_COMM_EXCHANGE_START, c->logical[kidx(c, j)], c->gpeer[g], nullptr, 0);
       if (rc) return rc;
       started = true;
       break;
@@ -752,17 +773,17 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
         // (its elementwise operand) in slot j+1 and let the pass read u instead
         const uint64_t nloc = 1ull << c->n;
         if (j > 0) {
-          CUDA_TRY(rsv::launch_scale(slot(c, j + 1), slot(c, j - 1), make_double2(prev_coef, 0.0), nloc, 0, c->st));
+          CUDA_TRY(rsv::launch_scale(kvec(c, j + 1), kvec(c, j - 1), make_double2(prev_coef, 0.0), nloc, 0, c->st));
         } else {
-          CUDA_TRY(cudaMemsetAsync(slot(c, j + 1), 0, sizeof(cplx) * nloc, c->st));
+          CUDA_TRY(cudaMemsetAsync(kvec(c, j + 1), 0, sizeof(cplx) * nloc, c->st));
         }
       }
       int rc = shard_before_last(c, j, sigma, started, p2p);
       if (rc) return rc;
     }
     if (p.chunk) {
-      int rc = launch_chunk_pass(c, p, omegas, deltas, slot(c, j), rsv::SC_SG + j, j > 0 ? slot(c, j - 1) : nullptr,
-                                 slot(c, j + 1), j);
+      int rc = launch_chunk_pass(c, p, omegas, deltas, kvec(c, j), rsv::SC_SG + j, j > 0 ? kvec(c, j - 1) : nullptr,
+                                 kvec(c, j + 1), j);
       if (rc) return rc;
       continue;
     }
@@ -772,7 +793,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     A.sh = p.sh;
     A.fl = flips_for(p, omegas, rsv::pass_threads_for(p.sh.a + p.sh.g, A.kind, p.sh.a));
     A.dg = diag_for(c, p, deltas);
-    A.x = slot(c, j);
+    A.x = kvec(c, j);
     A.x_scale_slot = rsv::SC_SG + j;
     A.j = j;
     A.sc = c->d_sc;
@@ -780,17 +801,17 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     A.counter = c->d_counter;
     // elementwise operand: -beta' s_{j-1} joins in the first pass, the partial sum u in the others
     if (pi == 0) {
-      A.ein = j > 0 ? slot(c, j - 1) : nullptr;
+      A.ein = j > 0 ? kvec(c, j - 1) : nullptr;
       A.ein_is_prev = 1;
       if (c->sharded && np == 1) {
-        A.ein = slot(c, j + 1);
+        A.ein = kvec(c, j + 1);
         A.ein_is_prev = 0;
       }
     } else {
-      A.ein = slot(c, j + 1);
+      A.ein = kvec(c, j + 1);
       A.ein_is_prev = 0;
     }
-    A.out = slot(c, j + 1);   // u in place, then s_{j+1}
+    A.out = kvec(c, j + 1);   // u in place, then s_{j+1}
     if (p2p && !last) {
       // the partner reads (NVLink) are spread over the passes before the last one so they overlap
       // more local work: active global qubit number i goes to pass i mod (np - 1)
@@ -798,7 +819,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
       for (size_t g = 0; g < c->gcoef.size(); ++g) {
         if (c->gcoef[g] == 0.0) continue;
         if (active++ % (int)(np - 1) != (int)pi) continue;
-        A.peer[A.npeer] = c->peer_slots[g][c->logical[j]];
+        A.peer[A.npeer] = c->peer_slots[g][c->logical[kidx(c, j)]];
         A.peer_coef[A.npeer] = c->gcoef[g];
         ++A.npeer;
       }
@@ -870,6 +891,59 @@ int reorthogonalize(rsv_context* c, int j, double n0, const std::vector<double>&
   return RSV_OK;
 }
 
+// Krylov combination when the basis outgrew the resident slots (k > K = cap): s_0..s_{K-2} are
+// resident, the ring (slots K-1, K) holds s_{k-1} and s_k. (1) psi = sum over the resident vectors
+// and s_{k-1}, in place in slot 0; (2) iterations K-2 .. k-3 are re-run (same kernels, same inputs:
+// the same vectors bit for bit) to regenerate s_{K-1} .. s_{k-2} through the ring, and every two of
+// them are added to psi by an in-place combination; the last one also carries the next step's
+// q-sweep, the norm and the observables.
+int combine_with_regeneration(rsv_context* c, int k, const std::vector<zc>& coef, const std::vector<double>& betas,
+                              const double* omegas, const double* deltas, const double* qo, const double* qd,
+                              int obs, double qoff) {
+  const int K = kcap(c);
+  cplx* psi = slot(c, 0);
+  {
+    std::vector<const cplx*> v;
+    std::vector<zc> cf;
+    for (int i = 0; i <= K - 2; ++i) {
+      v.push_back(kvec(c, i));
+      cf.push_back(coef[i]);
+    }
+    v.push_back(kvec(c, k - 1));
+    cf.push_back(coef[k - 1]);
+    int rc = run_combine(c, (int)v.size(), cf, psi, nullptr, nullptr, 0, 0.0, &v);
+    if (rc) return rc;
+  }
+  // regenerate s_{K-1} .. s_{k-2}: iteration j writes s_{j+1}
+  std::vector<int> pending;
+  for (int j = K - 2; j <= k - 3; ++j) {
+    const double sigma = betas[j - 1] > 0.0 ? 1.0 / betas[j - 1] : 0.0;   // j >= K-2 >= 1
+    const double sg_prev = j == 1 ? (c->n0sq_global > 0.0 ? 1.0 / std::sqrt(c->n0sq_global) : 0.0)
+                                  : (betas[j - 2] > 0.0 ? 1.0 / betas[j - 2] : 0.0);
+    int rc = launch_lanczos_iteration(c, j, omegas, deltas, sigma, -betas[j - 1] * sg_prev);
+    if (rc) return rc;
+    if (c->sharded) {
+      rc = shard_finish_iteration(c, j);
+      if (rc) return rc;
+    }
+    pending.push_back(j + 1);
+    const bool final = j + 1 == k - 2;
+    if (pending.size() == 2 || final) {
+      std::vector<const cplx*> v(1, psi);
+      std::vector<zc> cf(1, zc(1.0, 0.0));
+      for (int i : pending) {
+        v.push_back(kvec(c, i));
+        cf.push_back(coef[i]);
+      }
+      pending.clear();
+      rc = run_combine(c, (int)v.size(), cf, psi, final ? qo : nullptr, final ? qd : nullptr, final ? obs : 0,
+                       qoff, &v);
+      if (rc) return rc;
+    }
+  }
+  return RSV_OK;
+}
+
 // One Lanczos run on the resident state for a time step of dt_rest (<= the requested step).
 // Returns the fraction of dt_rest actually advanced (1 when converged on the full step, < 1
 // when the Krylov basis hit the HBM cap and the step was split).
@@ -899,23 +973,31 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
   double residual = INFINITY, n0 = 0.0, beta = 0.0;
   bool converged = false;
   int k = 0;
-  for (int j = 0;; ++j) {
-    const double sigma = j == 0 ? (c->n0sq_global > 0.0 ? 1.0 / std::sqrt(c->n0sq_global) : 0.0)
-                                : (betas.back() > 0.0 ? 1.0 / betas.back() : 0.0);
-    // -beta_{j-1} sigma_{j-1}: the coefficient of s_{j-1} in iteration j (sharded single-pass plans)
-    double prev_coef = 0.0;
-    if (j > 0) {
+  // Speculative launch (small registers, where the host round trip per iteration is comparable to
+  // the kernels): iteration j+1 is enqueued before the host tests iteration j, when its output slot
+  // s_{j+2} is resident (never a ring slot holding a basis vector the combination may still need).
+  // A speculative iteration after convergence is wasted GPU time but touches nothing in use.
+  const bool spec = !c->sharded && !c->reorth &&
+                    (c->speculate > 0 || (c->speculate < 0 && c->n <= kSpeculateMaxQubits));
+  int launched = 0;
+  auto enqueue = [&](int j) -> int {
+    // host copies of sigma_j and -beta_{j-1} sigma_{j-1} (sharded runs only: the global flips and
+    // single-pass plans; the kernels read the device scalars)
+    double sigma = 0.0, prev_coef = 0.0;
+    if (c->sharded)
+      sigma = j == 0 ? (c->n0sq_global > 0.0 ? 1.0 / std::sqrt(c->n0sq_global) : 0.0)
+                     : (betas.back() > 0.0 ? 1.0 / betas.back() : 0.0);
+    if (j > 0 && c->sharded) {
       const double sg_prev = j == 1 ? (c->n0sq_global > 0.0 ? 1.0 / std::sqrt(c->n0sq_global) : 0.0)
                                     : (betas[j - 2] > 0.0 ? 1.0 / betas[j - 2] : 0.0);
       prev_coef = -betas[j - 1] * sg_prev;
     }
-    rc = launch_lanczos_iteration(c, j, omegas, deltas, sigma, prev_coef);
-    if (rc) return rc;
+    int rc2 = launch_lanczos_iteration(c, j, omegas, deltas, sigma, prev_coef);
+    if (rc2) return rc2;
     if (c->sharded) {
-      rc = shard_finish_iteration(c, j);
-      if (rc) return rc;
+      rc2 = shard_finish_iteration(c, j);
+      if (rc2) return rc2;
     }
-    rep->matvecs += 1;
     CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_AL + j, c->d_sc + rsv::SC_AL + j, sizeof(double),
                              cudaMemcpyDeviceToHost, c->st));
     CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_BE + j, c->d_sc + rsv::SC_BE + j, sizeof(double),
@@ -923,7 +1005,21 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
     if (j == 0)
       CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_N0SQ, c->d_sc + rsv::SC_N0SQ, sizeof(double),
                                cudaMemcpyDeviceToHost, c->st));
-    CUDA_TRY(cudaStreamSynchronize(c->st));
+    CUDA_TRY(cudaEventRecord(c->iter_ev[j & 1], c->st));
+    ++launched;
+    return RSV_OK;
+  };
+  for (int j = 0;; ++j) {
+    if (launched == j) {
+      rc = enqueue(j);
+      if (rc) return rc;
+    }
+    if (spec && launched == j + 1 && j + 2 <= cap && j + 1 < kmax) {
+      rc = enqueue(j + 1);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaEventSynchronize(c->iter_ev[j & 1]));
+    rep->matvecs += 1;   // products the step uses (a discarded speculative iteration is not counted)
     prof_collect(c);
     if (j == 0) {
       n0 = std::sqrt(std::max(0.0, c->h_pin[rsv::SC_N0SQ]));
@@ -956,7 +1052,10 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
       break;
     }
     if (k >= kmax) break;                                       // krylov.py:114
-    if (k >= cap) break;                                        // HBM cap: split below
+    // resident-basis cap: continue in the slot ring and regenerate the overwritten vectors for the
+    // combination (exact: the same deterministic kernels recompute them bit for bit); the opt-in
+    // re-orthogonalisation needs the whole basis resident and splits the step in time instead
+    if (k >= (c->reorth || !c->tail_regen ? cap : kRegenMax) || (cap < 3 && k >= cap)) break;
     betas.push_back(beta);
   }
 
@@ -999,10 +1098,18 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
   const bool more = frac < 1.0;
   const double* qo = more ? omegas : q_omegas;
   const double* qd = more ? deltas : q_deltas;
-  // elementwise, so in place: every amplitude of s_0 is read before it is overwritten
-  rc = run_combine(c, k, coef, slot(c, 0), qo, qd, (!more && last_run && observe) ? 1 : 0,
-                   more ? c->offset : c->next_offset);
-  if (rc) return rc;
+  const int obs = (!more && last_run && observe) ? 1 : 0;
+  const double qoff = more ? c->offset : c->next_offset;
+  if (k <= cap) {
+    // elementwise, so in place: every amplitude of s_0 is read before it is overwritten
+    rc = run_combine(c, k, coef, slot(c, 0), qo, qd, obs, qoff);
+    if (rc) return rc;
+  } else {
+    rc = combine_with_regeneration(c, k, coef, betas, omegas, deltas, qo, qd, obs, qoff);
+    if (rc) return rc;
+    rep->regenerated += k - cap;
+    rep->matvecs += k - cap;
+  }
   if (qo != nullptr) {
     c->prep_key = prep_key_for(c, qo, qd, more ? c->offset : c->next_offset);
     c->prep_valid = true;
@@ -1098,6 +1205,8 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
 
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_pin, sizeof(double) * rsv::SC_SIZE);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->obs_event, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->iter_ev[0], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->iter_ev[1], cudaEventDisableTiming);
   if (e == cudaSuccess)
     e = cudaMemcpy(c->d_u, c->h_u.data(), sizeof(double) * n_qubits * n_qubits, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(c->d_counter, 0, sizeof(unsigned) * 4);
@@ -1127,6 +1236,8 @@ void rsv_destroy(rsv_context* c) {
   cudaFree(c->d_done);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->obs_event) cudaEventDestroy(c->obs_event);
+  for (cudaEvent_t ev : c->iter_ev)
+    if (ev) cudaEventDestroy(ev);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
@@ -1488,6 +1599,19 @@ int rsv_set_shard_peers(rsv_context* c, int n_global, const void* const* ptrs, i
 int rsv_shard_local_norm_sq(rsv_context* c, double* out) {
   if (!c || !out) return fail(RSV_ERR_ARG, "NULL argument");
   *out = c->local_n0sq;
+  return RSV_OK;
+}
+
+int rsv_set_speculation(rsv_context* c, int mode) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (mode < -1 || mode > 1) return fail(RSV_ERR_ARG, "speculation mode %d not in {-1, 0, 1}", mode);
+  c->speculate = mode;
+  return RSV_OK;
+}
+
+int rsv_set_tail_regeneration(rsv_context* c, int on) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  c->tail_regen = on != 0;
   return RSV_OK;
 }
 

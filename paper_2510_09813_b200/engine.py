@@ -83,6 +83,14 @@ class Context:
         """Full re-orthogonalisation of the Lanczos basis (reference krylov.py:103-104), opt-in."""
         nat.check(self.lib.rsv_set_reorthogonalize(self.ctx, 1 if on else 0), "rsv_set_reorthogonalize")
 
+    def set_tail_regeneration(self, on: bool):
+        """Beyond the resident basis: ring + regeneration (default) or exact split in time (off)."""
+        nat.check(self.lib.rsv_set_tail_regeneration(self.ctx, 1 if on else 0), "rsv_set_tail_regeneration")
+
+    def set_speculation(self, mode: int):
+        """Speculative launch of Lanczos iteration j+1 before j is tested: -1 auto (N <= 24), 0 off, 1 on."""
+        nat.check(self.lib.rsv_set_speculation(self.ctx, int(mode)), "rsv_set_speculation")
+
     def set_plan(self, chunk_group_bits: int = -1, chunk_lag: int = -1):
         """Pass-plan override (tests/tuning): -1 auto, 0 plain passes, 3..9 force the chunk pass."""
         nat.check(self.lib.rsv_set_plan(self.ctx, int(chunk_group_bits), int(chunk_lag)), "rsv_set_plan")

@@ -57,6 +57,7 @@ class KrylovReport:
     alpha0: float = float("nan")
     norm_in: float = float("nan")
     matvecs: int = 0
+    regenerated: int = 0   # Lanczos vectors recomputed because the basis outgrew the resident slots
 
 
 def _tridiag_exp_e1(alphas, betas, tau):
@@ -102,7 +103,7 @@ def _fused(slice_, psi, dt_ns, cfg):
     finally:
         eng.close()
     report = KrylovReport(rep.iterations, bool(rep.converged), float(rep.residual), 1 + rep.substeps,
-                          rep.alpha0, rep.norm_in, rep.matvecs)
+                          rep.alpha0, rep.norm_in, rep.matvecs, rep.regenerated)
     return (out.cpu().numpy() if was_numpy else out), report
 
 

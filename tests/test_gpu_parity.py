@@ -260,15 +260,72 @@ class TestEvolve:
         assert len(iters) == 300 and np.abs(iters - g["iterations"]).max() <= 1
 
     def test_krylov_cap_substepping_is_exact(self, rs, torch):
-        # a tiny HBM budget caps the Krylov basis; the step is split in time and must agree
+        # a tiny HBM budget caps the resident Krylov basis; the step is split in time (tail
+        # regeneration off) and must agree
+        from paper_2510_09813_b200.engine import SvEngine
+
         g = load("evolve_detmap12.npz")
         n = 12
         reg = rs.Register(tuple(map(tuple, g["positions"])), float(g["c6"]))
-        seq = rs.DiscretizedSequence(10, g["omegas"][:5], g["deltas"][:5], 50)
-        full = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12)))
-        capped = rs.evolve_sv(seq, reg, rs.SvRunConfig(krylov=rs.KrylovConfig(1e-12), krylov_vectors_cap=6))
-        assert any(r.substeps > 1 for r in capped.krylov_reports)
-        assert rs.norm_difference(full.final_state, capped.final_state) <= 1e-9
+        u = rs.interaction_matrix(reg)
+        full = SvEngine(n, u, krylov_vectors_cap=60)
+        capped = SvEngine(n, u, krylov_vectors_cap=6)
+        capped.set_tail_regeneration(False)
+        subs = 0
+        for k in range(5):
+            full.step(g["omegas"][k], g["deltas"][k], 10.0, 1e-12, 100)
+            subs += capped.step(g["omegas"][k], g["deltas"][k], 10.0, 1e-12, 100).substeps
+        assert subs > 0
+        assert rs.norm_difference(full.state(), capped.state()) <= 1e-9
+
+    @pytest.mark.parametrize("n,cap", [(12, 3), (12, 6), (22, 4), (22, 7)])
+    def test_tail_regeneration_matches_resident_basis(self, rs, torch, n, cap):
+        # beyond the resident basis the recurrence continues in a two-slot ring and the overwritten
+        # vectors are regenerated for the combination: same Krylov dimension per step as with the
+        # whole basis resident (the reference's k, krylov.py:96-117) and the same state to rounding
+        from paper_2510_09813_b200.engine import SvEngine
+
+        rng = np.random.default_rng(n + cap)
+        om, de, u = random_slice(rng, n)
+        full = SvEngine(n, u, krylov_vectors_cap=60)
+        capped = SvEngine(n, u, krylov_vectors_cap=cap)
+        for e in (full, capped):
+            e.set_speculation(0)
+        full.set_observables([1 << q for q in range(n)])
+        capped.set_observables([1 << q for q in range(n)])
+        regen = 0
+        for k in range(4):
+            dt = 6.0 + 3.0 * k
+            a = full.step(om, de, dt, 1e-12, 100, next_params=(om, de), observe=True)
+            b = capped.step(om, de, dt, 1e-12, 100, next_params=(om, de), observe=True)
+            assert a.converged and b.converged and b.substeps == 0
+            assert a.iterations == b.iterations and a.iterations > cap
+            assert b.regenerated == a.iterations - cap and b.matvecs == a.matvecs + b.regenerated
+            assert abs(a.alpha0 - b.alpha0) <= 1e-12 * max(1.0, abs(a.alpha0))
+            assert np.abs(full.observables() - capped.observables()).max() <= 1e-13
+            regen += b.regenerated
+        assert regen > 0
+        assert rs.norm_difference(full.state(), capped.state()) <= 1e-12
+        for e in (full, capped):
+            e.close()
+
+    @pytest.mark.parametrize("n", [10, 20])
+    def test_speculative_iterations_change_nothing(self, rs, torch, n):
+        # iteration j+1 launched before the host tests j (small N): the same kernels in the same
+        # order, so the same state bit for bit; the discarded iteration is not counted
+        from paper_2510_09813_b200.engine import SvEngine
+
+        rng = np.random.default_rng(40 + n)
+        om, de, u = random_slice(rng, n)
+        runs = []
+        for mode in (0, 1):
+            e = SvEngine(n, u, krylov_vectors_cap=60)
+            e.set_speculation(mode)
+            reps = [e.step(om, de, 5.0 + k, 1e-10, 100, next_params=(om, de)) for k in range(5)]
+            runs.append((e.state().cpu().numpy(), [(r.iterations, r.matvecs) for r in reps]))
+            e.close()
+        assert np.array_equal(runs[0][0], runs[1][0])
+        assert runs[0][1] == runs[1][1]
 
     def test_host_final_state_and_force_numpy_flag(self, rs):
         # SvRunConfig(host_final_state=True): numpy final state like the reference (sv.py:66), the
