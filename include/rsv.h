@@ -133,9 +133,17 @@ int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass:
 #define RSV_COMM_ALLREDUCE 1
 #define RSV_COMM_EXCHANGE_START 2
 #define RSV_COMM_EXCHANGE_WAIT 3
+#define RSV_COMM_ALLREDUCE_DEVICE 4   /* `host` is a DEVICE pointer into the buffer of rsv_set_shard_scratch:
+                                         enqueue an in-place sum all-reduce of `count` doubles on the context
+                                         stream (e.g. NCCL) and return without waiting for it */
 typedef int (*rsv_comm_fn)(void* user, int op, int slot, int peer, double* host, int count);
 int rsv_set_shard(rsv_context* ctx, rsv_comm_fn comm, void* user, void* exchange_buffer);   /* buffer may be NULL
                                                      in peer-memory mode (rsv_set_shard_peers) */
+/* Device scratch (>= 2 doubles) for on-stream all-reduces of the Lanczos scalars (RSV_COMM_ALLREDUCE_DEVICE):
+ * with it, a peer-memory sharded iteration has no host synchronisation (alpha's share before the last
+ * pass, ||w||^2 and q after it are reduced on the stream and finished by a device kernel). NULL: the
+ * host all-reduce path. */
+int rsv_set_shard_scratch(rsv_context* ctx, double* dev_buf, int count);
 /* This step's constant energy of the shard's global bits (and the next step's), and per global qubit
  * Omega_g/2 (0 = no flip) with the partner rank. */
 int rsv_set_shard_step(rsv_context* ctx, double offset, double next_offset, int n_global, const double* coef,

@@ -50,6 +50,7 @@ COMM_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c
 RSV_COMM_ALLREDUCE = 1
 RSV_COMM_EXCHANGE_START = 2
 RSV_COMM_EXCHANGE_WAIT = 3
+RSV_COMM_ALLREDUCE_DEVICE = 4
 
 # name -> (restype, argtypes); exactly the symbols declared in include/rsv.h
 SIGNATURES = {
@@ -90,6 +91,7 @@ SIGNATURES = {
     "rsv_set_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]),
     "rsv_set_reorthogonalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_tail_regeneration": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rsv_set_shard_scratch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_speculation": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_shard": (ctypes.c_int, [ctypes.c_void_p, COMM_FN, ctypes.c_void_p, ctypes.c_void_p]),
     "rsv_set_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int,

@@ -183,16 +183,22 @@ bool encode_tile_map(CUtensorMap* m, const void* base, const rsv::Shape& sh) {
   return r == CUDA_SUCCESS;
 }
 
-// Choose the tile-load mode of a pass and encode its TMA descriptors.
-void set_tile_load(rsv::PassArgs& A) {
+}  // namespace
+struct rsv_context;
+namespace {
+bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv::Shape& sh);
+
+// Choose the tile-load mode of a pass and set its TMA descriptors (encoded once per vector and
+// shape, rsv_context::maps).
+void set_tile_load(rsv_context* c, rsv::PassArgs& A) {
   const rsv::Shape& sh = A.sh;
   if (sh.g == 0) {
     A.load = rsv::LOAD_CONTIG;
     return;
   }
   A.load = rsv::LOAD_RUNS;
-  if (RSV_TENSOR_MAPS && sh.a <= 7 && encode_tile_map(&A.tm_x, A.x, sh) &&
-      (A.ein == nullptr || encode_tile_map(&A.tm_e, A.ein, sh)))
+  if (RSV_TENSOR_MAPS && sh.a <= 7 && cached_tile_map(c, &A.tm_x, A.x, sh) &&
+      (A.ein == nullptr || cached_tile_map(c, &A.tm_e, A.ein, sh)))
     A.load = rsv::LOAD_TENSOR;
 }
 
@@ -222,6 +228,16 @@ struct rsv_context {
   double* d_gc = nullptr;         // lo-pass tile table (per run)
   double* d_dvec = nullptr;
   double* h_pin = nullptr;
+  double* d_red = nullptr;          // sharded runs: caller's device buffer for on-stream all-reduces
+  int red_count = 0;                //   (rsv_set_shard_scratch; RSV_COMM_ALLREDUCE_DEVICE)
+  double* h_mail = nullptr;         // mapped pinned mailbox: [n0sq, alpha_0, beta_0, alpha_1, ...]
+  double* d_mail = nullptr;         //   its device address (written by the last pass)
+  struct MapEntry {
+    const void* base;
+    int n, a, p, g;
+    CUtensorMap map;
+  };
+  std::vector<MapEntry> maps;       // TMA descriptors by (vector, tile shape): encoded once
   std::vector<void*> phys;        // bound slots
   std::vector<int> logical;       // logical slot -> physical; logical 0..K = Krylov s_j, K+1 = work
   std::vector<PassPlan> plan;
@@ -267,6 +283,18 @@ struct rsv_context {
 };
 
 namespace {
+
+bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv::Shape& sh) {
+  for (const auto& e : c->maps)
+    if (e.base == base && e.n == sh.n && e.a == sh.a && e.p == sh.p && e.g == sh.g) {
+      *m = e.map;
+      return true;
+    }
+  if (!encode_tile_map(m, base, sh)) return false;
+  if (c->maps.size() >= 64) c->maps.clear();   // user vectors of rsv_apply_hamiltonian come and go
+  c->maps.push_back({base, sh.n, sh.a, sh.p, sh.g, *m});
+  return true;
+}
 
 // Slots 0..K: s_0 (the state) .. s_{K-1} are the Krylov basis; the partial sums u of iteration j
 // live in slot j+1 (each pass reads and rewrites its own tiles in place, the last pass turns u
@@ -586,6 +614,13 @@ int shard_before_last(rsv_context* c, int j, double sigma, bool started, bool p2
     dot = c->h_pin[rsv::SC_GF];
     add += cs * sigma * dot;
   }
+  if (p2p && c->d_red != nullptr) {   // on-stream all-reduce of alpha's partial share (no host sync)
+    CUDA_TRY(cudaMemcpyAsync(c->d_red, c->d_sc + rsv::SC_AP + j, sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    int rc = comm_call(c, RSV_COMM_ALLREDUCE_DEVICE, -1, -1, c->d_red, 1);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->d_sc + rsv::SC_AP + j, c->d_red, sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    return RSV_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(&c->h_pin[rsv::SC_AP + j], c->d_sc + rsv::SC_AP + j, sizeof(double),
                            cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -600,6 +635,15 @@ int shard_before_last(rsv_context* c, int j, double sigma, bool started, bool p2
 // After the (raw) last pass of iteration j: all-reduce ||w_j||^2 and <w_j|A_last|w_j>, write back
 // beta_j, sigma_{j+1}, q_{j+1}.
 int shard_finish_iteration(rsv_context* c, int j) {
+  if (c->d_red != nullptr && c->red_count >= 2) {   // on-stream: all-reduce + finishing kernel + mailbox
+    CUDA_TRY(cudaMemcpyAsync(c->d_red, c->d_sc + rsv::SC_BE + j, sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->d_red + 1, c->d_sc + rsv::SC_Q + j + 1, sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->st));
+    int rc = comm_call(c, RSV_COMM_ALLREDUCE_DEVICE, -1, -1, c->d_red, 2);
+    if (rc) return rc;
+    CUDA_TRY(rsv::launch_shard_scalars(c->d_sc, j, c->d_red, c->d_mail, c->st));
+    return RSV_OK;
+  }
   double* h = c->h_pin;
   CUDA_TRY(cudaMemcpyAsync(h + rsv::SC_BE + j, c->d_sc + rsv::SC_BE + j, sizeof(double), cudaMemcpyDeviceToHost,
                            c->st));
@@ -826,7 +870,8 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     }
     A.qsweep = last ? 1 : 0;
     A.raw = (last && c->sharded) ? 1 : 0;
-    set_tile_load(A);
+    A.mail = (last && !c->sharded) ? c->d_mail : nullptr;
+    set_tile_load(c, A);
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
@@ -891,12 +936,13 @@ int reorthogonalize(rsv_context* c, int j, double n0, const std::vector<double>&
   return RSV_OK;
 }
 
-// Krylov combination when the basis outgrew the resident slots (k > K = cap): s_0..s_{K-2} are
+// Krylov combination when the basis outgrew the resident slots (k > K = cap >= 4): s_0..s_{K-2} are
 // resident, the ring (slots K-1, K) holds s_{k-1} and s_k. (1) psi = sum over the resident vectors
 // and s_{k-1}, in place in slot 0; (2) iterations K-2 .. k-3 are re-run (same kernels, same inputs:
 // the same vectors bit for bit) to regenerate s_{K-1} .. s_{k-2} through the ring, and every two of
 // them are added to psi by an in-place combination; the last one also carries the next step's
-// q-sweep, the norm and the observables.
+// q-sweep, the norm and the observables. (K >= 4: the first re-run iteration reads s_{K-3} as its
+// previous vector, which must not be slot 0, where psi is being accumulated.)
 int combine_with_regeneration(rsv_context* c, int k, const std::vector<zc>& coef, const std::vector<double>& betas,
                               const double* omegas, const double* deltas, const double* qo, const double* qd,
                               int obs, double qoff) {
@@ -998,13 +1044,14 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
       rc2 = shard_finish_iteration(c, j);
       if (rc2) return rc2;
     }
-    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_AL + j, c->d_sc + rsv::SC_AL + j, sizeof(double),
-                             cudaMemcpyDeviceToHost, c->st));
-    CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_BE + j, c->d_sc + rsv::SC_BE + j, sizeof(double),
-                             cudaMemcpyDeviceToHost, c->st));
-    if (j == 0)
-      CUDA_TRY(cudaMemcpyAsync(c->h_pin + rsv::SC_N0SQ, c->d_sc + rsv::SC_N0SQ, sizeof(double),
+    if (c->sharded && c->d_red == nullptr) {   // scalars finished by the host (all-reduced): copy them
+      CUDA_TRY(cudaMemcpyAsync(c->h_mail + 1 + 2 * j, c->d_sc + rsv::SC_AL + j, sizeof(double),
                                cudaMemcpyDeviceToHost, c->st));
+      CUDA_TRY(cudaMemcpyAsync(c->h_mail + 2 + 2 * j, c->d_sc + rsv::SC_BE + j, sizeof(double),
+                               cudaMemcpyDeviceToHost, c->st));
+      if (j == 0)
+        CUDA_TRY(cudaMemcpyAsync(c->h_mail, c->d_sc + rsv::SC_N0SQ, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }   // else the last pass wrote them to the mapped mailbox
     CUDA_TRY(cudaEventRecord(c->iter_ev[j & 1], c->st));
     ++launched;
     return RSV_OK;
@@ -1021,11 +1068,12 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
     CUDA_TRY(cudaEventSynchronize(c->iter_ev[j & 1]));
     rep->matvecs += 1;   // products the step uses (a discarded speculative iteration is not counted)
     prof_collect(c);
+    const volatile double* mail = c->h_mail;
     if (j == 0) {
-      n0 = std::sqrt(std::max(0.0, c->h_pin[rsv::SC_N0SQ]));
+      n0 = std::sqrt(std::max(0.0, (double)mail[0]));
       if (first_run) {
         rep->norm_in = n0;
-        rep->alpha0 = c->h_pin[rsv::SC_AL];
+        rep->alpha0 = mail[1];
       }
       if (n0 <= norm_eps) {   // krylov.py:83-84: zero vector returned unchanged
         *zero_vector = true;
@@ -1033,8 +1081,8 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
         return RSV_OK;
       }
     }
-    alphas.push_back(c->h_pin[rsv::SC_AL + j]);
-    beta = c->h_pin[rsv::SC_BE + j];
+    alphas.push_back((double)mail[1 + 2 * j]);
+    beta = mail[2 + 2 * j];
     if (c->reorth) {
       rc = reorthogonalize(c, j, n0, betas, omegas, deltas, &beta);
       if (rc) return rc;
@@ -1055,7 +1103,7 @@ int lanczos_run(rsv_context* c, const double* omegas, const double* deltas, doub
     // resident-basis cap: continue in the slot ring and regenerate the overwritten vectors for the
     // combination (exact: the same deterministic kernels recompute them bit for bit); the opt-in
     // re-orthogonalisation needs the whole basis resident and splits the step in time instead
-    if (k >= (c->reorth || !c->tail_regen ? cap : kRegenMax) || (cap < 3 && k >= cap)) break;
+    if (k >= (c->reorth || !c->tail_regen ? cap : kRegenMax) || (cap < 4 && k >= cap)) break;
     betas.push_back(beta);
   }
 
@@ -1204,6 +1252,8 @@ int rsv_create(int n_qubits, const double* interaction_u, int diag_mode, void* s
   if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, sizeof(unsigned) * done_rows);
 
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_pin, sizeof(double) * rsv::SC_SIZE);
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->h_mail, sizeof(double) * (2 * 128 + 2), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&c->d_mail, c->h_mail, 0);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->obs_event, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->iter_ev[0], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->iter_ev[1], cudaEventDisableTiming);
@@ -1235,6 +1285,7 @@ void rsv_destroy(rsv_context* c) {
   cudaFree(c->d_dots);
   cudaFree(c->d_done);
   if (c->h_pin) cudaFreeHost(c->h_pin);
+  if (c->h_mail) cudaFreeHost(c->h_mail);
   if (c->obs_event) cudaEventDestroy(c->obs_event);
   for (cudaEvent_t ev : c->iter_ev)
     if (ev) cudaEventDestroy(ev);
@@ -1254,6 +1305,7 @@ int rsv_bind_slots(rsv_context* c, void* const* slots, int nslots) {
   if (nslots - 1 > rsv::kMaxKrylov)
     nslots = rsv::kMaxKrylov + 1;   // extra slots are never used
   c->phys.assign(slots, slots + nslots);
+  c->maps.clear();
   for (int i = 0; i < nslots; ++i) {
     if (c->phys[i] == nullptr || (reinterpret_cast<uintptr_t>(c->phys[i]) & 15u))
       return fail(RSV_ERR_ARG, "slot %d is NULL or not 16-byte aligned", i);
@@ -1324,7 +1376,7 @@ int rsv_apply_hamiltonian(rsv_context* c, const double* omegas, const double* de
     A.out = reinterpret_cast<cplx*>(out);
     A.ein = pi == 0 ? nullptr : reinterpret_cast<const cplx*>(out);
     A.ein_is_prev = 0;
-    set_tile_load(A);
+    set_tile_load(c, A);
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
@@ -1541,6 +1593,14 @@ int rsv_set_shard(rsv_context* c, rsv_comm_fn comm, void* user, void* exchange_b
   c->comm_user = user;
   c->xbuf = reinterpret_cast<cplx*>(exchange_buffer);
   c->prep_valid = false;
+  return RSV_OK;
+}
+
+int rsv_set_shard_scratch(rsv_context* c, double* dev_buf, int count) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (dev_buf != nullptr && count < 2) return fail(RSV_ERR_ARG, "the scratch buffer needs >= 2 doubles");
+  c->d_red = dev_buf;
+  c->red_count = dev_buf ? count : 0;
   return RSV_OK;
 }
 

@@ -143,6 +143,9 @@ struct alignas(64) PassArgs {
   const cplx* peer[4];                  //   read the partner shards' x over NVLink (P2P loads)
   double peer_coef[4];                  //   Omega_g / 2
   double* sc; double* part; unsigned* counter;
+  double* mail;                         // LAST_LANCZOS (not raw): mapped pinned host memory receiving
+                                        //   [n0sq (j=0)], alpha_j, beta_j -- the host reads them after the
+                                        //   iteration's event, no device-to-host copies in the stream
 };
 
 struct CombineArgs {
@@ -225,6 +228,7 @@ cudaError_t launch_chunk_norms(const cplx* psi, uint64_t n, double* sums, uint64
 cudaError_t launch_sample(const cplx* psi, uint64_t n, const double* prefix, uint64_t nchunks, const double* u,
                           double total, int64_t shots, int64_t* out, cudaStream_t st);
 cudaError_t launch_scale(cplx* y, const cplx* x, double2 a, uint64_t n, int grid, cudaStream_t st);
+cudaError_t launch_shard_scalars(double* sc, int j, const double* red, double* mail, cudaStream_t st);
 int max_grid_rows();   // upper bound on the grid of any kernel writing partial rows
 
 }  // namespace rsv

@@ -336,7 +336,8 @@ class FusedShardEngine:
     """
 
     def __init__(self, n_qubits: int, u, dist, *, device=None, max_krylov_dim: int = 100,
-                 memory_budget_bytes=None, krylov_vectors_cap=None, initial_local=None, peer_memory=False):
+                 memory_budget_bytes=None, krylov_vectors_cap=None, initial_local=None, peer_memory=False,
+                 device_scalars=True):
         import ctypes
 
         import torch
@@ -398,6 +399,13 @@ class FusedShardEngine:
         nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self._cb, None,
                                              self.xbuf.data_ptr() if self.xbuf is not None else None),
                   "rsv_set_shard")
+        # on-stream all-reduces of the per-iteration Lanczos scalars (RSV_COMM_ALLREDUCE_DEVICE): the
+        # peer-memory iteration then has no host round trip (device_scalars=False: host path)
+        self.red = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.device_scalars = bool(device_scalars)
+        if self.device_scalars:
+            nat.check(self.eng.lib.rsv_set_shard_scratch(self.eng.ctx, ctypes.c_void_p(self.red.data_ptr()), 8),
+                      "rsv_set_shard_scratch")
         self.eng.set_observables([1 << q for q in range(nl)])
         psi = self.eng.state()
         if initial_local is not None:   # this shard's amplitudes (host or device tensor)
@@ -452,7 +460,11 @@ class FusedShardEngine:
     def _comm(self, _user, op, slot, peer, host, count):
         try:
             torch, dist, nat = self.torch, self.dist, self.nat
-            if op == nat.RSV_COMM_ALLREDUCE:
+            if op == nat.RSV_COMM_ALLREDUCE_DEVICE:
+                # `host` points into self.red (device): in-place sum on the current stream (the
+                # context's); NCCL orders it with the stream's kernels, nothing waits on the host
+                dist.all_reduce(self.red[:count])
+            elif op == nat.RSV_COMM_ALLREDUCE:
                 arr = np.ctypeslib.as_array(host, shape=(count,))
                 t = torch.from_numpy(arr.copy())
                 if self.nccl:

@@ -278,7 +278,7 @@ class TestEvolve:
         assert subs > 0
         assert rs.norm_difference(full.state(), capped.state()) <= 1e-9
 
-    @pytest.mark.parametrize("n,cap", [(12, 3), (12, 6), (22, 4), (22, 7)])
+    @pytest.mark.parametrize("n,cap", [(12, 4), (12, 6), (22, 4), (22, 7)])
     def test_tail_regeneration_matches_resident_basis(self, rs, torch, n, cap):
         # beyond the resident basis the recurrence continues in a two-slot ring and the overwritten
         # vectors are regenerated for the combination: same Krylov dimension per step as with the
