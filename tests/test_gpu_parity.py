@@ -515,7 +515,7 @@ class TestMaxSize:
             om, de = seq.step(6)
             psi0 = eng.state().clone()
             rep = eng.step(om, de, 10.0, 1e-10, 100)
-            assert rep.converged and rep.substeps >= 1          # 6 resident vectors: split steps
+            assert rep.converged and rep.regenerated >= 1       # 6 resident vectors: ring + regeneration
             assert abs(math.sqrt(rs.overlap(eng.state(), eng.state()).real) - 1.0) <= 1e-9
             back = eng.step(om, de, -10.0, 1e-10, 100)
             assert back.converged
