@@ -57,7 +57,7 @@ PRELUDE = textwrap.dedent(f"""
             out, it, conv, res, alphas, _ = O.expm_multiply(lambda v: O.apply_hamiltonian(om, diag, v),
                                                              self.psi, dt, tol, kmax, eps)
             r = Rep()
-            r.iterations, r.residual, r.substeps, r.matvecs = it, res, 0, it
+            r.iterations, r.residual, r.substeps, r.matvecs, r.regenerated = it, res, 0, it, 0
             r.converged = int(conv and self.calls != FakeEngine.fail_at)
             r.alpha0 = alphas[0] if alphas else 0.0
             r.norm_in = float(np.linalg.norm(self.psi))
