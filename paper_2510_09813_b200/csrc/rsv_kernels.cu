@@ -162,12 +162,6 @@ __device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned
   return true;
 }
 
-// Reductions accumulate into NACC independent partial sums (by element index) so the per-tile
-// dot products are NACC short dependency chains instead of one long one (ncu: a single acc_q
-// chain of ~96 dependent DFMA per tile was the top "wait" stall of the last pass).
-constexpr int NACC = 4;
-__device__ __forceinline__ double sum_acc(const double (&a)[NACC]) { return (a[0] + a[1]) + (a[2] + a[3]); }
-
 template <int EPT>
 struct RegBits {
   static constexpr int value = EPT >= 16 ? 4 : (EPT >= 8 ? 3 : (EPT >= 4 ? 2 : (EPT >= 2 ? 1 : 0)));
@@ -275,7 +269,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
   #pragma unroll
   for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
   const double axs = alpha * xs;
-  double acc_a[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_n[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_q[NACC] = {0.0, 0.0, 0.0, 0.0};
+  double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
   // element i of a thread sits at index(t, tid) + i*S: the plan keeps the i*NT bits either all
   // contiguous (lo tile) or all in the strided group (hi tiles, a <= log2 NT)
   const uint64_t S = elem_offset(A.sh, NT);
@@ -394,7 +388,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;   // this pass's operator applied to v = xs * x
-      acc_a[i & (NACC - 1)] = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a[i & (NACC - 1)]));
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
         const cplx u = (RSV_EIN_REGS && KIND == PASS_MID) ? ev[i] : ubuf[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
@@ -403,7 +397,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
       if (LANCZOS) {
         cr = fma(-axs, xv[i].x, cr);
         ci = fma(-axs, xv[i].y, ci);
-        acc_n[i & (NACC - 1)] = fma(cr, cr, fma(ci, ci, acc_n[i & (NACC - 1)]));
+        acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
       ac[i] = make_double2(cr, ci);
       st_stream(po + i * S, ac[i]);
@@ -432,7 +426,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
           hr = fma(d, ac[i].x, hr);
           hi = fma(d, ac[i].y, hi);
         }
-        acc_q[i & (NACC - 1)] = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q[i & (NACC - 1)]));
+        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
       }
       for (int f = 0; f < A.fl.count; ++f) {
         const int m = A.fl.mask[f];
@@ -442,7 +436,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           const cplx p = ps[i * NT];
-          acc_q[i & (NACC - 1)] = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q[i & (NACC - 1)]);
+          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
         }
       }
     }
@@ -451,13 +445,13 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 #endif
   }
   cp_async_wait<0>();
-  for (int q = 0; q < NACC; ++q) acc_a[q] *= xs;
+  acc_a *= xs;
 
   if (KIND == PASS_LAST_APPLY) return;
   double mine[3];
-  mine[0] = block_sum<NT>(sum_acc(acc_a), red);
-  mine[1] = block_sum<NT>(sum_acc(acc_n), red);
-  mine[2] = block_sum<NT>(sum_acc(acc_q), red);
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = block_sum<NT>(acc_n, red);
+  mine[2] = block_sum<NT>(acc_q, red);
   double tot[3];
   if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
   if (threadIdx.x != 0) return;
@@ -506,7 +500,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   #pragma unroll
   for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
   const double axs = alpha * xs;
-  double acc_a[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_n[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_q[NACC] = {0.0, 0.0, 0.0, 0.0};
+  double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
   const uint64_t S = elem_offset(A.sh, NT);
   const uint64_t ntiles = A.sh.n_tiles;
   const uint64_t G = gridDim.x;
@@ -630,7 +624,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;
-      acc_a[i & (NACC - 1)] = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a[i & (NACC - 1)]));
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
         const cplx u = ebuf[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
@@ -639,7 +633,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
       if (LANCZOS) {
         cr = fma(-axs, xv[i].x, cr);
         ci = fma(-axs, xv[i].y, ci);
-        acc_n[i & (NACC - 1)] = fma(cr, cr, fma(ci, ci, acc_n[i & (NACC - 1)]));
+        acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
       ac[i] = make_double2(cr, ci);
       st_stream(po + i * S, ac[i]);
@@ -668,7 +662,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
           hr = fma(d, ac[i].x, hr);
           hi = fma(d, ac[i].y, hi);
         }
-        acc_q[i & (NACC - 1)] = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q[i & (NACC - 1)]));
+        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
       }
       for (int f = 0; f < A.fl.count; ++f) {
         const int m = A.fl.mask[f];
@@ -678,19 +672,19 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           const cplx p = ps[i * NT];
-          acc_q[i & (NACC - 1)] = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q[i & (NACC - 1)]);
+          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
         }
       }
       fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
     }
   }
-  for (int q = 0; q < NACC; ++q) acc_a[q] *= xs;
+  acc_a *= xs;
 
   if (KIND == PASS_LAST_APPLY) return;
   double mine[3];
-  mine[0] = block_sum<NT>(sum_acc(acc_a), red);
-  mine[1] = block_sum<NT>(sum_acc(acc_n), red);
-  mine[2] = block_sum<NT>(sum_acc(acc_q), red);
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = block_sum<NT>(acc_n, red);
+  mine[2] = block_sum<NT>(acc_q, red);
   double tot[3];
   if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
   if (threadIdx.x != 0) return;
@@ -734,7 +728,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   #pragma unroll
   for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
   const double axs = alpha * xs;
-  double acc_a[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_n[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_q[NACC] = {0.0, 0.0, 0.0, 0.0};
+  double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
   const uint64_t S = elem_offset(A.sh, NT);
   const uint64_t ntiles = A.sh.n_tiles;
   const uint64_t G = gridDim.x;
@@ -847,7 +841,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;
-      acc_a[i & (NACC - 1)] = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a[i & (NACC - 1)]));
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
         const cplx u = eb[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
@@ -856,7 +850,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
       if (LANCZOS) {
         cr = fma(-axs, xv[i].x, cr);
         ci = fma(-axs, xv[i].y, ci);
-        acc_n[i & (NACC - 1)] = fma(cr, cr, fma(ci, ci, acc_n[i & (NACC - 1)]));
+        acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
       ac[i] = make_double2(cr, ci);
       st_stream(po + i * S, ac[i]);
@@ -884,7 +878,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
           hr = fma(d, ac[i].x, hr);
           hi = fma(d, ac[i].y, hi);
         }
-        acc_q[i & (NACC - 1)] = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q[i & (NACC - 1)]));
+        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
       }
       // each pair (e, e^m) once: the partner with bit m clear takes the even amplitudes, the one
       // with bit m set the odd ones -- every thread works on every flip (no idle half-warps/warps)
@@ -897,20 +891,20 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
         for (int i = 0; i < EPT; ++i) {
           if ((i & 1) != own) continue;
           const cplx p = ps[i * NT];
-          acc_q[i & (NACC - 1)] = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q[i & (NACC - 1)]);
+          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
         }
       }
       fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
     }
     bx = bn;
   }
-  for (int q = 0; q < NACC; ++q) acc_a[q] *= xs;
+  acc_a *= xs;
 
   if (KIND == PASS_LAST_APPLY) return;
   double mine[3];
-  mine[0] = block_sum<NT>(sum_acc(acc_a), red);
-  mine[1] = block_sum<NT>(sum_acc(acc_n), red);
-  mine[2] = block_sum<NT>(sum_acc(acc_q), red);
+  mine[0] = block_sum<NT>(acc_a, red);
+  mine[1] = block_sum<NT>(acc_n, red);
+  mine[2] = block_sum<NT>(acc_q, red);
   double tot[3];
   if (!grid_finalize<3, NT>(mine, A.part, A.counter, tot, red)) return;
   if (threadIdx.x != 0) return;
@@ -1007,7 +1001,7 @@ __global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ Ch
   const double xs = sc[A.x_scale_slot];
   const bool has_prev = A.prev != nullptr;
   const double ecoef_m = has_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 0.0;
-  double acc_a[NACC] = {0.0, 0.0, 0.0, 0.0};
+  double acc_a = 0.0;
   const uint64_t Sm = elem_offset(A.shm, NT), Sl = elem_offset(A.shl, NT);
   const uint64_t nt = A.shl.n_tiles;
   const uint64_t total = 2 * nt;
@@ -1180,7 +1174,7 @@ __global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ Ch
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       double cr = ac[i].x, ci = ac[i].y;
-      acc_a[i & (NACC - 1)] = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a[i & (NACC - 1)]));
+      acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
       if (has_e) {
         const cplx u = ebuf[tid + i * NT];
         cr = fma(ecoef, u.x, cr);
@@ -1203,10 +1197,10 @@ __global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ Ch
     __syncthreads();
     if (tid == 0) red_release_gpu(A.done + signal_chunk, 1u);
   }
-  for (int q = 0; q < NACC; ++q) acc_a[q] *= xs;
+  acc_a *= xs;
 
   double mine[3];
-  mine[0] = block_sum<NT>(sum_acc(acc_a), red);
+  mine[0] = block_sum<NT>(acc_a, red);
   mine[1] = 0.0;
   mine[2] = 0.0;
   double tot[3];
@@ -1245,7 +1239,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
   double occ_p = 0.0, occ_r[RB > 0 ? RB : 1];
   #pragma unroll
   for (int b = 0; b < RB; ++b) occ_r[b] = 0.0;
-  double acc_n[NACC] = {0.0, 0.0, 0.0, 0.0}, acc_q[NACC] = {0.0, 0.0, 0.0, 0.0};
+  double acc_n = 0.0, acc_q = 0.0;
   uint64_t off[EPT];
   #pragma unroll
   for (int i = 0; i < EPT; ++i) off[i] = elem_offset(A.sh, i * NT);
@@ -1338,7 +1332,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       if (A.out != nullptr) st_stream(A.out + g0 + off[i], wv[i]);
-      acc_n[i & (NACC - 1)] = fma(wv[i].x, wv[i].x, fma(wv[i].y, wv[i].y, acc_n[i & (NACC - 1)]));
+      acc_n = fma(wv[i].x, wv[i].x, fma(wv[i].y, wv[i].y, acc_n));
     }
     if (A.qsweep) {
       DiagRow<NT, EPT> dr;
@@ -1361,7 +1355,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
           hr = fma(d, wv[i].x, hr);
           hi = fma(d, wv[i].y, hi);
         }
-        acc_q[i & (NACC - 1)] = fma(wv[i].x, hr, fma(wv[i].y, hi, acc_q[i & (NACC - 1)]));
+        acc_q = fma(wv[i].x, hr, fma(wv[i].y, hi, acc_q));
       }
       for (int f = 0; f < A.fl.count; ++f) {
         const int m = A.fl.mask[f];
@@ -1369,7 +1363,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           const cplx p = sw[(tid + i * NT) ^ m];
-          acc_q[i & (NACC - 1)] = fma(c, fma(wv[i].x, p.x, wv[i].y * p.y), acc_q[i & (NACC - 1)]);
+          acc_q = fma(c, fma(wv[i].x, p.x, wv[i].y * p.y), acc_q);
         }
       }
       __syncthreads();
@@ -1412,8 +1406,8 @@ __global__ void __launch_bounds__(NT, NT >= RSV_COMBINE_THREADS ? 1 : 2) combine
   cp_async_wait<0>();
 #endif
   double mine[2];
-  mine[0] = block_sum<NT>(sum_acc(acc_n), red);
-  mine[1] = block_sum<NT>(sum_acc(acc_q), red);
+  mine[0] = block_sum<NT>(acc_n, red);
+  mine[1] = block_sum<NT>(acc_q, red);
   constexpr int stride = 2 + kMaxMasks;
   if (tid == 0) {
     A.part[(size_t)blockIdx.x * stride + 0] = mine[0];

@@ -47,7 +47,7 @@ def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False):
         np.save(os.path.join(outdir, "occ.npy"), occ)
         np.save(os.path.join(outdir, "in.npy"), {"pos": list(reg.positions_um), "om": om, "de": de,
                                                  "iters": [r.iterations for r in reps],
-                                                 "sub": [r.substeps for r in reps]}, allow_pickle=True)
+                                                 "sub": [r.substeps + r.regenerated for r in reps]}, allow_pickle=True)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -58,7 +58,7 @@ def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False):
                                               (2, 15, 6, True), (4, 24, None, True)])
 def test_fused_sharded_evolution(tmp_path, world, n, cap, peer):
     # (4, 14): 12 local qubits -> one lo pass carries the diagonal, the shard offset and the q-sweep;
-    # (2, 17): 16 local qubits -> lo + one group pass; cap 6 forces exact sub-stepping across shards;
+    # (2, 17): 16 local qubits -> lo + one group pass; cap 6 forces ring + regeneration across shards;
     # peer=True: peer-memory mode (the first passes read the partner shards' slots through CUDA IPC --
     # here on the same device, over NVLink on a multi-GPU box); (4, 24): 22 local qubits, three passes,
     # the two global qubits' partner reads split over the lo and mid passes
@@ -118,7 +118,7 @@ def _full_worker(rank, world, port, outdir, n, k0, steps, cap):
     ov = _probe_overlap(psi, rank * psi.numel())
     nsq = float(torch.sum(torch.abs(psi) ** 2).item())
     np.save(os.path.join(outdir, f"f{rank}.npy"), {"ov": ov, "nsq": nsq, "occ": occ, "peer": info["peer_memory"],
-                                                   "sub": sum(r.substeps for r in reps)}, allow_pickle=True)
+                                                   "sub": sum(r.substeps + r.regenerated for r in reps)}, allow_pickle=True)
     del psi
     dist.barrier()
     dist.destroy_process_group()
