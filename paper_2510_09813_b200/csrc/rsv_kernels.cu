@@ -727,6 +727,9 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   double rc[RB > 0 ? RB : 1];
   #pragma unroll
   for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
+  double r2[RB > 0 ? RB : 1];   // q-sweep: 2 Omega_b / 2 of the register bits
+  #pragma unroll
+  for (int b = 0; b < RB; ++b) r2[b] = 2.0 * A.fl.rcoef[b];
   const double axs = alpha * xs;
   double acc_a = 0.0, acc_n = 0.0, acc_q = 0.0;
   const uint64_t S = elem_offset(A.sh, NT);
@@ -863,36 +866,45 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
       #pragma unroll
       for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
       __syncthreads();
+      // <w|A_last|w> = sum over flip pairs (e, e^m) of 2 c Re(conj(w_e) w_{e^m}) (+ <w|D|w>):
+      // register bits pair the thread's own amplitudes (per-bit sums, scaled once)
       #pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        double hr = 0.0, hi = 0.0;
-        #pragma unroll
-        for (int b = 0; b < RB; ++b) {
-          if ((i >> b) & 1) continue;
-          hr = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].x, hr);
-          hi = fma(2.0 * A.fl.rcoef[b], ac[i ^ (1 << b)].y, hi);
-        }
-        if (DIAG) {
-          double d = dr.d[i];
-          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
-          hr = fma(d, ac[i].x, hr);
-          hi = fma(d, ac[i].y, hi);
-        }
-        acc_q = fma(ac[i].x, hr, fma(ac[i].y, hi, acc_q));
-      }
-      // each pair (e, e^m) once: the partner with bit m clear takes the even amplitudes, the one
-      // with bit m set the odd ones -- every thread works on every flip (no idle half-warps/warps)
-      for (int f = 0; f < A.fl.count; ++f) {
-        const int m = A.fl.mask[f];
-        const int own = (tid & m) ? 1 : 0;
-        const cplx* ps = sw + (tid ^ m);
-        const double c2 = 2.0 * A.fl.coef[f];
+      for (int b = 0; b < RB; ++b) {
+        double s0 = 0.0, s1 = 0.0;
         #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-          if ((i & 1) != own) continue;
-          const cplx p = ps[i * NT];
-          acc_q = fma(c2, fma(ac[i].x, p.x, ac[i].y * p.y), acc_q);
+          if ((i >> b) & 1) continue;
+          const cplx& q = ac[i ^ (1 << b)];
+          if (i & 1) s1 = fma(ac[i].x, q.x, fma(ac[i].y, q.y, s1));
+          else s0 = fma(ac[i].x, q.x, fma(ac[i].y, q.y, s0));
         }
+        acc_q = fma(r2[b], s0 + s1, acc_q);
+      }
+      if (DIAG) {
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          double d = dr.d[i];
+          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+          acc_q = fma(d, fma(ac[i].x, ac[i].x, ac[i].y * ac[i].y), acc_q);
+        }
+      }
+      // shared-memory bits: each pair (e, e^m) once -- the partner with bit m clear takes the even
+      // amplitudes, the one with bit m set the odd ones (selects instead of predication, so no issue
+      // slot is spent on masked-off lanes), per-flip sums scaled once
+      for (int f = 0; f < A.fl.count; ++f) {
+        const int m = A.fl.mask[f];
+        const bool own = (tid & m) != 0;
+        const cplx* ps = sw + (tid ^ m) + (own ? NT : 0);
+        double s0 = 0.0, s1 = 0.0;
+        #pragma unroll
+        for (int k = 0; k < EPT / 2; ++k) {
+          const cplx p = ps[2 * k * NT];
+          const double wx = own ? ac[2 * k + 1].x : ac[2 * k].x;
+          const double wy = own ? ac[2 * k + 1].y : ac[2 * k].y;
+          if (k & 1) s1 = fma(wx, p.x, fma(wy, p.y, s1));
+          else s0 = fma(wx, p.x, fma(wy, p.y, s0));
+        }
+        acc_q = fma(2.0 * A.fl.coef[f], s0 + s1, acc_q);
       }
       fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
     }
