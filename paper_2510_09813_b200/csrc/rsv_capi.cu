@@ -192,14 +192,19 @@ bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv
 // shape, rsv_context::maps).
 void set_tile_load(rsv_context* c, rsv::PassArgs& A) {
   const rsv::Shape& sh = A.sh;
+  A.tstore = 0;
   if (sh.g == 0) {
     A.load = rsv::LOAD_CONTIG;
+    A.tstore = A.out != nullptr ? 1 : 0;   // one bulk copy per output tile
     return;
   }
   A.load = rsv::LOAD_RUNS;
   if (RSV_TENSOR_MAPS && sh.a <= 7 && cached_tile_map(c, &A.tm_x, A.x, sh) &&
-      (A.ein == nullptr || cached_tile_map(c, &A.tm_e, A.ein, sh)))
+      (A.ein == nullptr || cached_tile_map(c, &A.tm_e, A.ein, sh))) {
     A.load = rsv::LOAD_TENSOR;
+    // output tiles by TMA tensor stores through the same tile geometry
+    if (A.out != nullptr && cached_tile_map(c, &A.tm_o, A.out, sh)) A.tstore = 1;
+  }
 }
 
 struct PassPlan {
@@ -291,7 +296,7 @@ bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv
       return true;
     }
   if (!encode_tile_map(m, base, sh)) return false;
-  if (c->maps.size() >= 64) c->maps.clear();   // user vectors of rsv_apply_hamiltonian come and go
+  if (c->maps.size() >= 512) c->maps.clear();   // user vectors of rsv_apply_hamiltonian come and go
   c->maps.push_back({base, sh.n, sh.a, sh.p, sh.g, *m});
   return true;
 }

@@ -36,6 +36,19 @@
 #ifndef RSV_EIN_REGS
 #define RSV_EIN_REGS 0
 #endif
+// output tiles leave through shared memory by TMA stores (PassArgs::tstore) instead of STG: in the
+// last pass (rotating buffers, w is staged in shared memory for the q-sweep anyway) and, opt-in, in
+// the lo/mid passes (measured slower there: the store delays the operand refill of the e buffer)
+#ifndef RSV_TSTORE
+#define RSV_TSTORE 1
+#endif
+#ifndef RSV_TSTORE_TMA
+#define RSV_TSTORE_TMA 0
+#endif
+// last pass: the q-sweep's shared-memory bits 4..7 as register pairs of a transposed layout
+#ifndef RSV_QT
+#define RSV_QT 1
+#endif
 
 namespace rsv {
 
@@ -84,6 +97,34 @@ __device__ __forceinline__ void tma_load_5d(void* smem_dst, const CUtensorMap* m
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// ---- TMA stores (shared -> global, bulk-group completion)
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2,
+                                             int c3, int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                 "r"(c4) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the source buffers of every committed store have been read (the buffer may be refilled)
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// every committed store is complete
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Output tile tt of a pass leaves shared memory (src, tile order e) by one TMA store; issued by one
+// thread after a CTA barrier that follows every writer's fence.proxy.async.
+__device__ __forceinline__ void store_tile(const PassArgs& A, uint64_t tt, const void* src) {
+  if (A.load == LOAD_CONTIG) {
+    bulk_s2g(A.out + ((uint64_t)tt << (A.sh.a + A.sh.g)), src, (unsigned)(sizeof(cplx) << (A.sh.a + A.sh.g)));
+  } else {
+    const int m = A.sh.p - A.sh.a;
+    tma_store_5d(&A.tm_o, src, 0, (int)(tt & ((1ull << m) - 1ull)), 0, 0, (int)(tt >> m));
+  }
+  bulk_commit();
 }
 
 __device__ __forceinline__ cplx ld_stream(const cplx* p) {
@@ -539,6 +580,9 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   }
   __syncthreads();
   unsigned xphase = 0u, ephase = 0u;   // bit s = parity of x stage s (a register, not a local array)
+  // output tiles through the e buffer (in place over the operand) and a TMA store issued at the
+  // next tile barrier (no per-thread global stores, no 64-bit address arithmetic per amplitude)
+  const bool tstore = RSV_TSTORE_TMA && A.tstore != 0;
   // prologue: tile blockIdx.x into stage 0
   if (blockIdx.x < ntiles) {
     if (tid == 0) mbar_arrive_expect_tx(&bars[0], tile_bytes);
@@ -561,6 +605,15 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
     if (tn < ntiles) {
       issue(A.x, &A.tm_x, tn, xbuf + (stage ^ 1) * TILE, &bars[stage ^ 1]);
       if (DIAG && tid == 0) bulk_g2s(rows + (stage ^ 1) * 16, A.dg.gc + tn * kGcStride, 112, &bars[stage ^ 1]);
+    }
+    if (tstore && t != blockIdx.x) {
+      // tile t-G's output sits in the e buffer: store it and let it be read before the refill
+      if (tid == 0) {
+        store_tile(A, t - G, ebuf);
+        bulk_wait_read0();
+      }
+      // without an operand nothing else orders this tile's epilogue writes after the store's reads
+      if (!has_e) __syncthreads();
     }
     if (has_e) issue(A.ein, &A.tm_e, t, ebuf, &bars[2]);
     const cplx* s = xbuf + stage * TILE;
@@ -636,16 +689,20 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
         acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
       ac[i] = make_double2(cr, ci);
-      st_stream(po + i * S, ac[i]);
+      if (tstore) ebuf[tid + i * NT] = ac[i];   // over this thread's own operand entry
+      else st_stream(po + i * S, ac[i]);
     }
+    if (tstore) fence_proxy_async_smem();   // generic writes -> the TMA store's reads
 
     if (LANCZOS && A.qsweep) {
       // w goes to the e buffer: each thread overwrites only the entries it alone has read,
       // so a single barrier (w complete) suffices; the next refill of the buffer is issued
       // after the next tile barrier
       cplx* sw = ebuf;
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
+      if (!tstore) {
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
+      }
       __syncthreads();
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
@@ -676,6 +733,14 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
         }
       }
       fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
+    }
+  }
+  if (tstore && blockIdx.x < ntiles) {
+    __syncthreads();   // the CTA's last output tile is complete in the e buffer
+    if (tid == 0) {
+      const uint64_t tl = blockIdx.x + ((ntiles - 1 - blockIdx.x) / G) * G;
+      store_tile(A, tl, ebuf);
+      bulk_wait0();
     }
   }
   acc_a *= xs;
@@ -735,6 +800,22 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   const uint64_t S = elem_offset(A.sh, NT);
   const uint64_t ntiles = A.sh.n_tiles;
   const uint64_t G = gridDim.x;
+  const bool tstore = RSV_TSTORE && A.tstore != 0;
+  // q-sweep flips on tile bits 4..7 in a transposed layout (4096-amplitude tile, 16 per thread)
+  constexpr bool kQT = RSV_QT && TB == 12 && NT == 256;
+  unsigned qt_mask = 0u;
+  double qc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (kQT) {
+    for (int f = 0; f < A.fl.count; ++f) {
+      const int m = A.fl.mask[f];
+      #pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (m == (16 << b)) {
+          qt_mask |= (unsigned)m;
+          qc[b] = 2.0 * A.fl.coef[f];
+        }
+    }
+  }
 
   const int R = (1 << A.sh.a) < 32 ? (1 << A.sh.a) : (NT < 32 ? NT : 32);
   const int RUNS = (NT < 32 ? NT : 32) / R;
@@ -791,7 +872,10 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
     mbar_wait(&bars[bx], (phase >> bx) & 1u);
     phase ^= 1u << bx;
     __syncthreads();   // (A) everyone is past tile it-1: its operand buffer (= bn) is free
-    if (tn < ntiles) issue_x(tn, bn);
+    if (tn < ntiles) {
+      if (tstore && tid == 0) bulk_wait_read0();   // ... once the TMA store of w(it-1) has read it
+      issue_x(tn, bn);
+    }
     const cplx* s = buf + bx * TILE;
     DiagRow<NT, EPT> dr;
     if (DIAG) dr.setup(A.dg, A.sh, t, tid, rows + bx * 16);
@@ -836,6 +920,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
       issue(A.ein, &A.tm_e, tn, buf + bx * TILE, &bars[bx]);
     }
     const cplx* eb = buf + be * TILE;
+    cplx* sw = buf + be * TILE;   // the same buffer receives w(it)
     if (has_e) {
       mbar_wait(&bars[be], (phase >> be) & 1u);
       phase ^= 1u << be;
@@ -856,16 +941,23 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
         acc_n = fma(cr, cr, fma(ci, ci, acc_n));
       }
       ac[i] = make_double2(cr, ci);
-      st_stream(po + i * S, ac[i]);
+      if (tstore) sw[tid + i * NT] = ac[i];   // over this thread's own operand entry
+      else st_stream(po + i * S, ac[i]);
+    }
+    if (tstore) {
+      fence_proxy_async_smem();   // generic writes -> the TMA store's reads
+      __syncthreads();            // w(it) complete in the operand buffer
+      if (tid == 0) store_tile(A, t, sw);
     }
 
     if (LANCZOS && A.qsweep && !RSV_QSWEEP_OFF) {
       // w goes to the operand buffer of this tile (refilled only after the next barrier A);
       // without an operand that buffer is idle
-      cplx* sw = buf + be * TILE;
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
-      __syncthreads();
+      if (!tstore) {
+        #pragma unroll
+        for (int i = 0; i < EPT; ++i) sw[tid + i * NT] = ac[i];
+        __syncthreads();
+      }
       // <w|A_last|w> = sum over flip pairs (e, e^m) of 2 c Re(conj(w_e) w_{e^m}) (+ <w|D|w>):
       // register bits pair the thread's own amplitudes (per-bit sums, scaled once)
       #pragma unroll
@@ -893,6 +985,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
       // slot is spent on masked-off lanes), per-flip sums scaled once
       for (int f = 0; f < A.fl.count; ++f) {
         const int m = A.fl.mask[f];
+        if (qt_mask & m) continue;   // done below in the transposed layout
         const bool own = (tid & m) != 0;
         const cplx* ps = sw + (tid ^ m) + (own ? NT : 0);
         double s0 = 0.0, s1 = 0.0;
@@ -906,10 +999,35 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
         }
         acc_q = fma(2.0 * A.fl.coef[f], s0 + s1, acc_q);
       }
+      if constexpr (kQT) {
+        // tile bits 4..7 become register bits: thread tid reads w at e = (tid & 15) | (tid >> 4) << 8
+        // | i << 4 (8 consecutive lanes still cover 128 contiguous bytes: conflict free), so each of
+        // these flips costs one 16-byte load per amplitude for all four bits instead of a half load
+        // per bit
+        if (qt_mask != 0u) {
+          const cplx* w2p = sw + (tid & 15) + ((tid >> 4) << 8);
+          cplx w2[16];
+          #pragma unroll
+          for (int i = 0; i < 16; ++i) w2[i] = w2p[i << 4];
+          #pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            double s0 = 0.0, s1 = 0.0;
+            #pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if ((i >> b) & 1) continue;
+              const cplx& q = w2[i ^ (1 << b)];
+              if (i & 1) s1 = fma(w2[i].x, q.x, fma(w2[i].y, q.y, s1));
+              else s0 = fma(w2[i].x, q.x, fma(w2[i].y, q.y, s0));
+            }
+            acc_q = fma(qc[b], s0 + s1, acc_q);
+          }
+        }
+      }
       fence_proxy_async_smem();   // generic writes to a buffer the TMA engine refills later
     }
     bx = bn;
   }
+  if (tstore && tid == 0) bulk_wait0();   // the last output tile is written before the CTA exits
   acc_a *= xs;
 
   if (KIND == PASS_LAST_APPLY) return;

@@ -125,7 +125,11 @@ enum TileLoad : int {
 struct alignas(64) PassArgs {
   CUtensorMap tm_x;                     // TMA descriptors (LOAD_TENSOR) for x and ein
   CUtensorMap tm_e;
+  CUtensorMap tm_o;                     // ... and for out (tstore with LOAD_TENSOR)
   int load;                             // TileLoad
+  int tstore;                           // output tiles leave through shared memory by TMA stores
+                                        // (LOAD_CONTIG: bulk copy, LOAD_TENSOR: tm_o) instead of
+                                        // per-thread 16-byte global stores
   Shape sh;
   FlipSet fl;
   DiagArgs dg;
