@@ -250,20 +250,26 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+NCU_SUMMARIES = ("r2_ncu_n29_last_tstore.json",      # the last pass as it is now (TMA stores, round 2)
+                 "r2_ncu_n29_before_tstore.json",    # lo / mid / combine (unchanged since)
+                 "r1_ncu_n29_summary.json")
+
+
 def ncu_traffic(family, n, plan):
-    """DRAM bytes per launch of `family` from the committed ncu --set full summary (profiles/),
-    when it was captured for this N and pass plan; else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_n29_summary.json")) as fh:
-            d = json.load(fh)
-    except Exception:
-        return None, None
-    if d.get("n") != n or d.get("plan", "plain") != plan:
-        return None, None
-    k = d.get("kernels", {}).get(family)
-    if not k or "traffic_bytes" not in k:
-        return None, None
-    return int(k["traffic_bytes"]), k.get("kernel")
+    """DRAM bytes per launch of `family` from the newest committed ncu --set full summary
+    (profiles/) that captured this N, pass plan and kernel family; else None."""
+    for name in NCU_SUMMARIES:
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                d = json.load(fh)
+        except Exception:
+            continue
+        if d.get("n") != n or d.get("plan", "plain") != plan:
+            continue
+        k = d.get("kernels", {}).get(family)
+        if k and "traffic_bytes" in k:
+            return int(k["traffic_bytes"]), k.get("kernel"), name
+    return None, None, None
 
 
 def alg_bytes_per_launch(family, n, k_avg, diag):
@@ -517,7 +523,8 @@ def run_ours(args):
     achieved = alg / (avg_launch_ms / 1e3) / 1e9
     kernel_launches = int(sum(v["launches"] for v in prof.values()))
     plan_name = "chunk" if plan and plan[0].get("family") == "chunk" else "plain"
-    traffic, traffic_kernel = ncu_traffic(fam, n, plan_name) if args.diag == "fly" else (None, None)
+    traffic, traffic_kernel, traffic_file = (ncu_traffic(fam, n, plan_name) if args.diag == "fly"
+                                               else (None, None, None))
     pass_ms = {f: round(v["ms"], 3) for f, v in prof.items()}
 
     # ---- e2e through the public API: host initial state in, host final state + occupations out
@@ -616,7 +623,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm_peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
                          "traffic": traffic,
-                         "traffic_source": ("profiles/r1_ncu_n29_summary.json (dram__bytes_read.sum + "
+                         "traffic_source": (f"profiles/{traffic_file} (dram__bytes_read.sum + "
                                             f"dram__bytes_write.sum of one {traffic_kernel} launch)"
                                             if traffic else None),
                          "alg_bytes_per_launch": alg, "avg_launch_ms": avg_launch_ms},
