@@ -119,6 +119,13 @@ int rsv_lanczos_update(rsv_context* ctx, void* w, const void* v, const void* vpr
 int rsv_axpy(rsv_context* ctx, void* y, const void* x, double a_re, double a_im, uint64_t n);
 int rsv_scale(rsv_context* ctx, void* y, const void* x, double a_re, double a_im, uint64_t n);
 
+/* exp(-i tau T) e1 of the k x k Lanczos tridiagonal T (diagonal alphas[0..k), off-diagonal betas[0..k-1)),
+ * host only, no context; the function the step driver uses (Chebyshev expansion on the Gershgorin
+ * interval). Replaces rydsim/krylov.py:54 _tridiag_exp_e1 (dense eigh). full != 0: all k components (the
+ * Krylov combination's coefficients), out_re_im[2k]; full == 0: only the last one (what the convergence
+ * test krylov.py:107-111 reads), out_re_im[2]. */
+int rsv_tridiag_exp_e1(const double* alphas, const double* betas, int k, double tau, int full, double* out_re_im);
+
 /* Introspection / measurement support. */
 int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass: a, p, g, lo, family, chunk_gm] */
 /* Sharding by the top log2(P) qubits (north-star row e; paper_2510_09813_b200/sharding.py). The context

@@ -11,6 +11,8 @@ import ctypes
 import os
 import threading
 
+import numpy as np
+
 from .errors import RydsimError, SolverError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -87,6 +89,8 @@ SIGNATURES = {
                                 ctypes.c_double, ctypes.c_uint64]),
     "rsv_scale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_uint64]),
+    "rsv_tridiag_exp_e1": (ctypes.c_int, [c_double_p, c_double_p, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                          c_double_p]),
     "rsv_pass_plan": (ctypes.c_int, [ctypes.c_void_p, c_int_p, ctypes.c_int]),
     "rsv_set_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]),
     "rsv_set_reorthogonalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
@@ -147,3 +151,17 @@ def check(rc: int, what: str = ""):
 def dptr(arr):
     """ctypes double* for a contiguous float64 numpy array."""
     return arr.ctypes.data_as(c_double_p)
+
+
+def tridiag_exp_e1(alphas, betas, tau, full=True):
+    """exp(-1j tau T) e1 of the Lanczos tridiagonal through rsv_tridiag_exp_e1 (the step driver's own
+    function; krylov.py:54). full=False returns only the last component (as a 1-element array)."""
+    lib = load()
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    k = a.shape[0]
+    b = np.ascontiguousarray(betas, dtype=np.float64)[: max(k - 1, 0)]
+    out = np.zeros(2 * k if full else 2)
+    rc = lib.rsv_tridiag_exp_e1(dptr(a), dptr(b) if k > 1 else None, k, float(tau), 1 if full else 0, dptr(out))
+    check(rc, "rsv_tridiag_exp_e1")
+    return out[0::2] + 1j * out[1::2]
+

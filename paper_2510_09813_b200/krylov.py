@@ -61,16 +61,8 @@ class KrylovReport:
 
 
 def _tridiag_exp_e1(alphas, betas, tau):
-    """exp(-1j tau T) e1 on the host (k <= 100 scalars; krylov.py:54)."""
-    k = len(alphas)
-    if k == 1:
-        return np.array([np.exp(-1j * tau * alphas[0])])
-    t = np.diag(np.asarray(alphas, dtype=float))
-    off = np.arange(k - 1)
-    t[off, off + 1] = betas
-    t[off + 1, off] = betas
-    lam, z = np.linalg.eigh(t)
-    return z @ (np.exp(-1j * tau * lam) * z[0, :])
+    """exp(-1j tau T) e1 on the host (krylov.py:54), by the step driver's own routine (rsv_tridiag_exp_e1)."""
+    return nat.tridiag_exp_e1(alphas, betas, tau)
 
 
 def _fused(slice_, psi, dt_ns, cfg):

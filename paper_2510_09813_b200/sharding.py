@@ -27,6 +27,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native as nat
 from .errors import MemoryBudgetError, ValidationError
 
 NS_TO_US = 1e-3
@@ -112,15 +113,8 @@ class ShardedOperator:
 
 
 def tridiag_exp_e1(alphas, betas, tau):
-    k = len(alphas)
-    if k == 1:
-        return np.array([np.exp(-1j * tau * alphas[0])])
-    t = np.diag(np.asarray(alphas, dtype=float))
-    idx = np.arange(k - 1)
-    t[idx, idx + 1] = betas
-    t[idx + 1, idx] = betas
-    lam, z = np.linalg.eigh(t)
-    return z @ (np.exp(-1j * tau * lam) * z[0, :])
+    """exp(-1j tau T) e1 (krylov.py:54) by the step driver's routine (rsv_tridiag_exp_e1)."""
+    return nat.tridiag_exp_e1(alphas, betas, tau)
 
 
 def sharded_expm_multiply(op: ShardedOperator, psi, dt_ns, tolerance=1e-10, max_krylov_dim=100,

@@ -50,6 +50,28 @@ class TestCAbi:
         assert rc == _native.RSV_ERR_CUDA
         assert b"no CPU fallback" in lib.rsv_last_error() or b"CUDA" in lib.rsv_last_error()
 
+    @pytest.mark.parametrize("k", [1, 2, 3, 7, 20, 38, 60, 120])
+    def test_tridiagonal_exponential_vs_oracle(self, k):
+        # host-only entry point (no GPU): the Lanczos tridiagonal exp(-i tau T) e1 of krylov.py:54 by the
+        # driver's Chebyshev expansion, against the oracle's dense-eigh restatement: every component
+        # (full=1, the combination coefficients) and the last one alone (full=0, the convergence test)
+        from oracle import sv_oracle as O
+
+        lib = _native.load()
+        rng = np.random.default_rng(k)
+        for scale, tau in ((30.0, 0.01), (1500.0, 0.01), (800.0, -0.004), (5.0, 0.0)):
+            a = rng.uniform(-scale, scale, k)
+            b = rng.uniform(0.1 * scale, 0.6 * scale, max(k - 1, 0))
+            ref = O.tridiag_exp_e1(a, b, tau)
+            out = np.zeros(2 * k)
+            bp = _native.dptr(b) if k > 1 else None
+            assert lib.rsv_tridiag_exp_e1(_native.dptr(a), bp, k, tau, 1, _native.dptr(out)) == 0
+            full = out[0::2] + 1j * out[1::2]
+            assert np.abs(full - ref).max() <= 1e-12
+            last = np.zeros(2)
+            assert lib.rsv_tridiag_exp_e1(_native.dptr(a), bp, k, tau, 0, _native.dptr(last)) == 0
+            assert abs(complex(last[0], last[1]) - ref[-1]) <= 1e-13
+
     def test_product_never_imports_oracle(self):
         pkg = os.path.join(ROOT, "paper_2510_09813_b200")
         for root, _, files in os.walk(pkg):
