@@ -275,6 +275,7 @@ def ncu_traffic(family, n, plan):
 def alg_bytes_per_launch(family, n, k_avg, diag):
     """Algorithmic HBM bytes of one launch of a kernel family ('Roofline accounting').
 
+    iter2: lo + last in one launch (fused two-pass iteration)
     lo   : read s_j (16 B) + s_{j-1} (16 B, all but the first iteration of a step) + write u (16 B)
            (+ 8 B of precomputed diagonal for diag='vec')
     chunk: the same bytes for two bit groups (its second tile pass re-reads s_j and u' from L2)
@@ -283,6 +284,9 @@ def alg_bytes_per_launch(family, n, k_avg, diag):
     combine : read the k basis vectors, write psi ((k + 1) x 16 B)
     """
     amp = 2 ** n
+    if family == "iter2":   # fused [lo, last] iteration (13..21 qubits): both passes' bytes
+        prev_frac = (k_avg - 1.0) / k_avg if k_avg > 0 else 0.0
+        return (32 + 16 * prev_frac + (8 if diag == "vec" else 0) + 48) * amp
     if family in ("lo", "chunk", "first"):
         prev_frac = (k_avg - 1.0) / k_avg if k_avg > 0 else 0.0
         return (32 + 16 * prev_frac + (8 if diag == "vec" else 0)) * amp

@@ -127,7 +127,8 @@ int rsv_scale(rsv_context* ctx, void* y, const void* x, double a_re, double a_im
 int rsv_tridiag_exp_e1(const double* alphas, const double* betas, int k, double tau, int full, double* out_re_im);
 
 /* Introspection / measurement support. */
-int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass: a, p, g, lo, family, chunk_gm] */
+int rsv_pass_plan(rsv_context* ctx, int* out, int max_ints);   /* [np, per pass: a, p, g, lo, family, chunk_gm];
+                                                                   family 0 lo, 1 mid, 2 last, 3 fused [lo, last] */
 /* Sharding by the top log2(P) qubits (north-star row e; paper_2510_09813_b200/sharding.py). The context
  * is created for the LOCAL qubits (n - log2 P) with the local interaction block; per step the host passes
  * the shard's effective detunings as `deltas` of rsv_expm_step and the rest through rsv_set_shard_step.
@@ -176,6 +177,10 @@ int rsv_set_tail_regeneration(rsv_context* ctx, int on);
  * round trip on small registers; a speculative iteration after convergence is discarded):
  * -1 auto (N <= 24, the default), 0 off, 1 on. Never in sharded or re-orthogonalised runs. */
 int rsv_set_speculation(rsv_context* ctx, int mode);
+/* Run a two-pass Lanczos iteration ([lo, last] plans: 16..21 local qubits, single GPU) as one cooperative
+ * launch with a grid barrier between the passes: -1 auto (default: every such plan), 0 off, 1 on.
+ * Reference counterpart: none (launch latency). Its kernel time is reported under profile family 0. */
+int rsv_set_fusion(rsv_context* ctx, int mode);
 
 /* Full re-orthogonalisation of every new Lanczos vector against the basis (the reference algorithm,
  * krylov.py:103-104; classical Gram-Schmidt, two extra passes over the basis per iteration). Off by

@@ -97,6 +97,7 @@ SIGNATURES = {
     "rsv_set_tail_regeneration": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_shard_scratch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_speculation": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rsv_set_fusion": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rsv_set_shard": (ctypes.c_int, [ctypes.c_void_p, COMM_FN, ctypes.c_void_p, ctypes.c_void_p]),
     "rsv_set_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                           c_double_p, c_int_p]),

@@ -56,6 +56,7 @@ constexpr double kBreakdownRtol = 1e-14;  // krylov.py:25
 constexpr int kScratchJ = 127;            // alpha-partial slot used by plain H.psi
 constexpr int kRegenMax = rsv::kMaxKrylov; // Lanczos vectors of one run (device scalar arrays hold 128)
 constexpr int kSpeculateMaxQubits = 24;    // auto speculation: Lanczos iterations of <= ~0.5 ms
+constexpr int kFuseMaxQubits = 21;         // auto fused two-pass iteration (every 2-pass plan)
 constexpr int kPartStride = 2 * rsv::kMaxKrylov > 2 + rsv::kMaxMasks ? 2 * rsv::kMaxKrylov
                                                                       : 2 + rsv::kMaxMasks;   // widest partial row
 
@@ -268,6 +269,7 @@ struct rsv_context {
   bool reorth = false;              // full re-orthogonalisation (krylov.py:103-104), opt-in
   bool tail_regen = true;           // beyond the resident basis: ring + regeneration (else split in time)
   int speculate = -1;               // launch iteration j+1 before testing j: -1 auto (N <= 24), 0 off, 1 on
+  int fuse = -1;                    // two-pass plans in one cooperative launch: -1 auto (N <= 21), 0 off, 1 on
   cudaEvent_t iter_ev[2] = {nullptr, nullptr};
   double* d_dots = nullptr;         // <s_i|w> scratch (2 kMaxKrylov doubles)
   int plan_gm = -1;               // chunk group bits: -1 auto, 0 off, 3..9 forced (rsv_set_plan)
@@ -801,9 +803,48 @@ int launch_chunk_pass(rsv_context* c, const PassPlan& p, const double* omegas, c
   return RSV_OK;
 }
 
+// The plan is [lo, last] with 4096-amplitude tiles and the context may run it as one cooperative
+// launch (iter2_kernel): single-GPU runs of 16..21 qubits.
+bool fused_iteration(const rsv_context* c) {
+  if (c->fuse == 0 || c->sharded || c->plan.size() != 2) return false;
+  const PassPlan& lo = c->plan[0];
+  const PassPlan& last = c->plan[1];
+  if (!lo.lo || lo.chunk || lo.sh.a + lo.sh.g != rsv::kLoBits || last.sh.a + last.sh.g != rsv::kLoBits) return false;
+  if (last.sh.a > rsv::ilog2(RSV_LAST_THREADS)) return false;   // a thread's amplitudes at one stride
+  return c->fuse > 0 || c->n <= kFuseMaxQubits;
+}
+
 int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const double* deltas, double sigma,
                              double prev_coef) {
   const size_t np = c->plan.size();
+  if (fused_iteration(c)) {
+    rsv::Iter2Args F{};
+    for (int pi = 0; pi < 2; ++pi) {
+      rsv::PassArgs& A = pi == 0 ? F.lo : F.last;
+      const PassPlan& p = c->plan[pi];
+      A.kind = pi == 0 ? rsv::PASS_FIRST : rsv::PASS_LAST_LANCZOS;
+      A.sh = p.sh;
+      A.fl = flips_for(p, omegas, RSV_LAST_THREADS);
+      A.dg = diag_for(c, p, deltas);
+      A.x = kvec(c, j);
+      A.x_scale_slot = rsv::SC_SG + j;
+      A.j = j;
+      A.sc = c->d_sc;
+      A.part = c->d_part;
+      A.counter = c->d_counter;
+      A.ein = pi == 0 ? (j > 0 ? kvec(c, j - 1) : nullptr) : kvec(c, j + 1);
+      A.ein_is_prev = pi == 0 ? 1 : 0;
+      A.out = kvec(c, j + 1);
+      A.qsweep = pi == 1 ? 1 : 0;
+      A.mail = pi == 1 ? c->d_mail : nullptr;
+      set_tile_load(c, A);
+    }
+    F.gridbar = c->d_counter + 2;
+    prof_begin(c, 0);
+    CUDA_TRY(rsv::launch_iter2(F, c->st));
+    prof_end(c);
+    return RSV_OK;
+  }
   // sharded: start the first global-qubit exchange of s_j so it overlaps the local passes
   // (peer-memory mode: no exchange, the first pass reads the partner shards directly)
   bool started = false;
@@ -1595,7 +1636,7 @@ int rsv_pass_plan(rsv_context* c, int* out, int max_ints) {
     out[2 + 6 * i] = c->plan[i].sh.p;
     out[3 + 6 * i] = c->plan[i].sh.g;
     out[4 + 6 * i] = c->plan[i].lo ? 1 : 0;
-    out[5 + 6 * i] = family_of(i, np);
+    out[5 + 6 * i] = fused_iteration(c) ? 3 : family_of(i, np);   // 3: both passes in iter2_kernel
     out[6 + 6 * i] = c->plan[i].chunk ? c->plan[i].gm : 0;
   }
   return RSV_OK;
@@ -1690,6 +1731,13 @@ int rsv_set_speculation(rsv_context* c, int mode) {
   if (!c) return fail(RSV_ERR_ARG, "NULL context");
   if (mode < -1 || mode > 1) return fail(RSV_ERR_ARG, "speculation mode %d not in {-1, 0, 1}", mode);
   c->speculate = mode;
+  return RSV_OK;
+}
+
+int rsv_set_fusion(rsv_context* c, int mode) {
+  if (!c) return fail(RSV_ERR_ARG, "NULL context");
+  if (mode < -1 || mode > 1) return fail(RSV_ERR_ARG, "fusion mode %d not in {-1, 0, 1}", mode);
+  c->fuse = mode;
   return RSV_OK;
 }
 

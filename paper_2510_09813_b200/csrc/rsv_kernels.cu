@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 //   e buf  : this tile's elementwise operand, requested after the same barrier, awaited
 //            just before the epilogue
 template <int TB, int KIND, int NT, bool DIAG>
-__global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2) pass_kernel_tma(const __grid_constant__ PassArgs A) {
+__device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -536,12 +536,13 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   __shared__ double red[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // scalars through L2 (__ldcg): in the fused iteration kernel another CTA wrote them this launch
   const double* sc = A.sc;
-  const double xs = sc[A.x_scale_slot];
+  const double xs = __ldcg(sc + A.x_scale_slot);
   double alpha = 0.0;
-  if (LANCZOS) alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
+  if (LANCZOS) alpha = __ldcg(sc + SC_AP + A.j) + __ldcg(sc + SC_Q + A.j);
   const bool has_e = A.ein != nullptr;
-  const double ecoef = A.ein_is_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 1.0;
+  const double ecoef = A.ein_is_prev ? -(__ldcg(sc + SC_BE + A.j - 1) * __ldcg(sc + SC_SG + A.j - 1)) : 1.0;
   double rc[RB > 0 ? RB : 1];
   #pragma unroll
   for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
@@ -782,7 +783,7 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
 // that load has a whole epilogue plus the next tile's flips to land; the operand buffer of tile it
 // receives x(it+2) after the next tile barrier (A). Cost: one more CTA barrier per tile.
 template <int TB, int KIND, int NT, bool DIAG>
-__global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2) pass_kernel_rot(const __grid_constant__ PassArgs A) {
+__device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -795,12 +796,12 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   __shared__ double red[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* sc = A.sc;
-  const double xs = sc[A.x_scale_slot];
+  const double* sc = A.sc;   // through L2: see pass_tma_body
+  const double xs = __ldcg(sc + A.x_scale_slot);
   double alpha = 0.0;
-  if (LANCZOS) alpha = sc[SC_AP + A.j] + sc[SC_Q + A.j];
+  if (LANCZOS) alpha = __ldcg(sc + SC_AP + A.j) + __ldcg(sc + SC_Q + A.j);
   const bool has_e = A.ein != nullptr;
-  const double ecoef = A.ein_is_prev ? -(sc[SC_BE + A.j - 1] * sc[SC_SG + A.j - 1]) : 1.0;
+  const double ecoef = A.ein_is_prev ? -(__ldcg(sc + SC_BE + A.j - 1) * __ldcg(sc + SC_SG + A.j - 1)) : 1.0;
   double rc[RB > 0 ? RB : 1];
   #pragma unroll
   for (int b = 0; b < RB; ++b) rc[b] = A.fl.rcoef[b] * xs;
@@ -1064,6 +1065,17 @@ __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_
   } else {
     lanczos_scalars(scw, A.j, A.raw, alpha, tot[1], tot[2], A.mail);
   }
+}
+
+template <int TB, int KIND, int NT, bool DIAG>
+__global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2)
+    pass_kernel_tma(const __grid_constant__ PassArgs A) {
+  pass_tma_body<TB, KIND, NT, DIAG>(A);
+}
+template <int TB, int KIND, int NT, bool DIAG>
+__global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2)
+    pass_kernel_rot(const __grid_constant__ PassArgs A) {
+  pass_rot_body<TB, KIND, NT, DIAG>(A);
 }
 
 // ---------------------------------------------------------------- L2-resident chunk pass
@@ -1360,6 +1372,33 @@ __global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ Ch
     *A.ticket = 0ull;
     A.sc[SC_AP + A.j] = tot[0];
   }
+}
+
+// ---------------------------------------------------------------- fused two-pass Lanczos iteration
+// Registers of 16..21 qubits have two passes per iteration (lo, last; 4096-amplitude tiles) over a state that lives in
+// L2; each pass is then a few tiles per SM, so launch latency, the pipeline fill and the tail of
+// the grid reduction are a large part of it. One cooperative launch runs both: the lo pass, a grid
+// barrier (after it the lo pass's alpha share and every partial sum u are visible), the last pass.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_gpu(bar) < gridDim.x) __nanosleep(32);
+    fence_proxy_async_global();   // other CTAs' generic writes (u) -> this CTA's TMA reads
+  }
+  __syncthreads();
+  fence_proxy_async_smem();
+}
+
+template <bool DIAG>
+__global__ void __launch_bounds__(RSV_LAST_THREADS, 1) iter2_kernel(const __grid_constant__ Iter2Args A) {
+  pass_tma_body<kLoBits, PASS_FIRST, RSV_LAST_THREADS, DIAG>(A.lo);
+  grid_barrier(A.gridbar);
+  pass_rot_body<kLoBits, PASS_LAST_LANCZOS, RSV_LAST_THREADS, false>(A.last);
+  // second arrival: the last CTA to get here resets the barrier for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(A.gridbar, 1u) == 2u * gridDim.x - 1u) *A.gridbar = 0u;
 }
 
 // ---------------------------------------------------------------- Krylov combination
@@ -2031,6 +2070,26 @@ cudaError_t launch_chunk_d(const ChunkArgs& args, cudaStream_t st) {
   return launch_persistent(chunk_kernel<NT, DIAG>, args, 2 * args.shl.n_tiles, NT, smem, &occ, st);
 }
 
+template <bool DIAG>
+cudaError_t launch_iter2_d(const Iter2Args& args, cudaStream_t st) {
+  constexpr int NT = RSV_LAST_THREADS;
+  constexpr size_t smem = 3 * (1 << kLoBits) * sizeof(cplx) + 48 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+  auto kern = iter2_kernel<DIAG>;
+  static int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
+  }
+  const uint64_t tiles = std::max(args.lo.sh.n_tiles, args.last.sh.n_tiles);
+  const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;   // every CTA resident: the grid barrier
+  const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+  void* params[] = {const_cast<Iter2Args*>(&args)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NT), params, smem, st);
+}
+
 template <int TB>
 cudaError_t launch_combine_tb(const CombineArgs& args, cudaStream_t st) {
   constexpr int NT = combine_threads(TB);
@@ -2040,6 +2099,12 @@ cudaError_t launch_combine_tb(const CombineArgs& args, cudaStream_t st) {
 }
 
 }  // namespace
+
+cudaError_t launch_iter2(const Iter2Args& args, cudaStream_t st) {
+  if (args.lo.sh.a + args.lo.sh.g != kLoBits || args.last.sh.a + args.last.sh.g != kLoBits)
+    return cudaErrorInvalidValue;
+  return args.lo.dg.mode != DIAG_NONE ? launch_iter2_d<true>(args, st) : launch_iter2_d<false>(args, st);
+}
 
 cudaError_t launch_pass(const PassArgs& args, cudaStream_t st) {
   switch (args.sh.a + args.sh.g) {

@@ -198,6 +198,14 @@ struct alignas(64) ChunkArgs {
   unsigned* done;                       // per-chunk finished M tiles (reset by the last CTA)
 };
 
+// Fused two-pass Lanczos iteration (plans of exactly [lo, last] with 4096-amplitude tiles, 16..21 qubits):
+// both passes in one cooperative launch with a grid barrier between them (iter2_kernel).
+struct alignas(64) Iter2Args {
+  PassArgs lo;                          // PASS_FIRST, flips for RSV_LAST_THREADS threads
+  PassArgs last;                        // PASS_LAST_LANCZOS
+  unsigned* gridbar;                    // zero between launches
+};
+
 struct MultiDotArgs {
   const cplx* v[kMaxKrylov];
   const cplx* w;
@@ -211,6 +219,7 @@ struct MultiDotArgs {
 cudaError_t launch_pass(const PassArgs& args, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& args, cudaStream_t st);
 cudaError_t launch_chunk(const ChunkArgs& args, cudaStream_t st);
+cudaError_t launch_iter2(const Iter2Args& args, cudaStream_t st);
 cudaError_t launch_multidot(const MultiDotArgs& args, cudaStream_t st);
 cudaError_t launch_build_dl(int a, int n, const double* umat, const double* delta_host, int with_interaction,
                             double offset, double* dl, cudaStream_t st);

@@ -73,7 +73,7 @@ class Context:
         out = []
         for i in range(n):
             a, p, g, lo, fam, gm = (buf[1 + 6 * i + k] for k in range(6))
-            d = dict(a=a, p=p, g=g, lo=bool(lo), family=("lo", "mid", "last")[fam])
+            d = dict(a=a, p=p, g=g, lo=bool(lo), family=("lo", "mid", "last", "iter2")[fam])
             if gm:
                 d.update(family="chunk", chunk_bits=12 + gm, m_tile=dict(a=12 - gm, p=12, g=gm))
             out.append(d)
@@ -90,6 +90,11 @@ class Context:
     def set_speculation(self, mode: int):
         """Speculative launch of Lanczos iteration j+1 before j is tested: -1 auto (N <= 24), 0 off, 1 on."""
         nat.check(self.lib.rsv_set_speculation(self.ctx, int(mode)), "rsv_set_speculation")
+
+    def set_fusion(self, mode: int):
+        """Two-pass Lanczos iterations ([lo, last] plans, 16..21 qubits) in one cooperative launch:
+        -1 auto (on), 0 off, 1 on."""
+        nat.check(self.lib.rsv_set_fusion(self.ctx, int(mode)), "rsv_set_fusion")
 
     def set_plan(self, chunk_group_bits: int = -1, chunk_lag: int = -1):
         """Pass-plan override (tests/tuning): -1 auto, 0 plain passes, 3..9 force the chunk pass."""
@@ -225,6 +230,6 @@ class SvEngine(Context):
         cnt = (ctypes.c_longlong * 4)()
         nat.check(self.lib.rsv_get_profile(self.ctx, ms, cnt))
         p0 = self.pass_plan()[0]
-        first = "chunk" if p0["family"] == "chunk" else ("lo" if p0["lo"] else "first")
+        first = p0["family"] if p0["family"] in ("chunk", "iter2") else ("lo" if p0["lo"] else "first")
         names = (first, "mid", "last", "combine")
         return {names[i]: {"ms": ms[i], "launches": cnt[i]} for i in range(4)}

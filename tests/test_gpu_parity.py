@@ -327,6 +327,29 @@ class TestEvolve:
         assert np.array_equal(runs[0][0], runs[1][0])
         assert runs[0][1] == runs[1][1]
 
+    @pytest.mark.parametrize("n", [16, 18, 21])
+    def test_fused_iteration_matches_separate_passes(self, rs, torch, n):
+        # [lo, last] plans with 4096-amplitude tiles (16..21 qubits) run each Lanczos iteration as one cooperative launch
+        # (iter2_kernel: lo pass, grid barrier, last pass); against the two separate launches
+        from paper_2510_09813_b200.engine import SvEngine
+
+        rng = np.random.default_rng(60 + n)
+        om, de, u = random_slice(rng, n)
+        runs = []
+        for mode in (0, 1):
+            e = SvEngine(n, u, krylov_vectors_cap=60)
+            e.set_fusion(mode)
+            assert e.pass_plan()[0]["family"] == ("iter2" if mode else "lo")
+            e.set_observables([1 << q for q in range(n)])
+            reps = [e.step(om, de, 5.0 + k, 1e-10, 100, next_params=(om, de), observe=True) for k in range(4)]
+            runs.append((e.state().cpu().numpy(), [(r.iterations, r.matvecs) for r in reps], e.observables(),
+                         reps[-1].alpha0))
+            e.close()
+        assert runs[0][1] == runs[1][1]
+        assert np.linalg.norm(runs[0][0] - runs[1][0]) <= 1e-11
+        assert np.abs(runs[0][2] - runs[1][2]).max() <= 1e-12
+        assert abs(runs[0][3] - runs[1][3]) <= 1e-11 * max(1.0, abs(runs[0][3]))
+
     def test_host_final_state_and_force_numpy_flag(self, rs):
         # SvRunConfig(host_final_state=True): numpy final state like the reference (sv.py:66), the
         # workspace released; force_numpy_matvec (sv.py:61) is accepted and changes nothing

@@ -27,7 +27,7 @@ for k in range(3, 3 + steps):
     mv += r.matvecs
 prof = eng.profile()
 amp = 2 ** n
-alg = {"lo": 48 * amp, "first": 48 * amp, "chunk": 48 * amp, "mid": 48 * amp, "last": 48 * amp}   # x + elementwise operand + out
+alg = {"lo": 48 * amp, "first": 48 * amp, "chunk": 48 * amp, "mid": 48 * amp, "last": 48 * amp, "iter2": 96 * amp}   # x + elementwise operand + out
 out = {"lib": os.environ.get("RSV_LIB", "default"), "n": n, "matvecs": mv, "gm": os.environ.get("RSV_PLAN_GM", "-1"), "lag": os.environ.get("RSV_PLAN_LAG", "-1")}
 for f, v in prof.items():
     if v["launches"] and f in alg:

@@ -34,7 +34,7 @@ for k in range(first, first + steps):
     p = eng.profile()
     row = {"step": k, "k": r.iterations, "regen": r.regenerated, "split": r.substeps, "mv": r.matvecs}
     for f, v in p.items():
-        key = "lo" if f in ("lo", "first", "chunk") else f
+        key = "lo" if f in ("lo", "first", "chunk", "iter2") else f
         d_ms = v["ms"] - prev[key][0]
         d_n = v["launches"] - prev[key][1]
         prev[key] = (v["ms"], v["launches"])
