@@ -362,6 +362,7 @@ def run_sharded(args, rank, world, local, pg):
     achieved = alg / (avg_launch_ms / 1e3) / 1e9
     hbm_peak, peak_kind = peaks()
     krylov_cap = eng.eng.krylov_cap
+    peer_passes = eng.peer_stats()
     eng.close()
     del eng
     torch.cuda.ipc_collect()
@@ -401,12 +402,13 @@ def run_sharded(args, rank, world, local, pg):
         pulse_fields = {"s_per_us_pulse_extrapolated": ms / args.steps * seq.step_count / 1e3 / pulse_us,
                         "pulse_measured_s": None}
     # self-check of the multi-GPU run: the communicator saw every rank, one GPU per rank, and the mode
-    # (peer-memory P2P loads or exchange) that actually ran
+    # (peer memory: TMA ring or P2P loads; or exchange) that actually ran
     devs = [None] * world
     dist.all_gather_object(devs, (torch.cuda.current_device(), torch.cuda.get_device_properties(local).uuid.hex
                                   if hasattr(torch.cuda.get_device_properties(local), "uuid") else str(local)))
     mg_check = {"backend": dist.get_backend(), "world": dist.get_world_size(), "requested": args.gpus,
                 "distinct_gpus": len({d[1] for d in devs}), "peer_memory": bool(peer_mode),
+                "peer_passes": peer_passes,   # partner tiles by TMA ring / per-thread P2P loads
                 "ok": dist.get_world_size() == args.gpus}
     if rank == 0:
         line = {

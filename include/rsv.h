@@ -164,6 +164,9 @@ int rsv_set_shard_peers(rsv_context* ctx, int n_global, const void* const* ptrs,
 /* Make a (mapped) device pointer of another GPU readable from kernels on the current device
  * (cudaDeviceEnablePeerAccess; a no-op on the same device). */
 int rsv_enable_peer_access(const void* ptr);
+/* Peer-memory passes launched so far: out[0] with the partner tiles moved by TMA into a shared-memory
+ * ring, out[1] with per-thread P2P loads (tiles below 4096 amplitudes, RSV_PEER_TMA=0). */
+int rsv_shard_peer_stats(rsv_context* ctx, long long* out2);
 /* This shard's share of ||psi||^2 from the last Krylov combination / measurement. */
 int rsv_shard_local_norm_sq(rsv_context* ctx, double* out);
 

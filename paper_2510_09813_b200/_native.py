@@ -103,6 +103,7 @@ SIGNATURES = {
                                           c_double_p, c_int_p]),
     "rsv_shard_local_norm_sq": (ctypes.c_int, [ctypes.c_void_p, c_double_p]),
     "rsv_enable_peer_access": (ctypes.c_int, [ctypes.c_void_p]),
+    "rsv_shard_peer_stats": (ctypes.c_int, [ctypes.c_void_p, c_ll_p]),
     "rsv_set_shard_peers": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                            ctypes.c_int]),
     "rsv_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

@@ -12,6 +12,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -190,10 +191,26 @@ bool encode_tile_map(CUtensorMap* m, const void* base, const rsv::Shape& sh) {
   return r == CUDA_SUCCESS;
 }
 
+// The same tile geometry with the group split as [g-3 rows | 3 eighth bits]: the box is one eighth
+// of a tile (coordinate 3 selects it), the unit of the peer-memory TMA ring (PassArgs::tm_peer).
+bool encode_eighth_map(CUtensorMap* m, const void* base, const rsv::Shape& sh) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr || sh.a > 7 || sh.g < 3 || sh.g - 3 > 8 || base == nullptr) return false;
+  const int g1 = sh.g - 3, hb = sh.n - sh.p - sh.g;
+  cuuint64_t dim[5] = {2ull << sh.a, 1ull << (sh.p - sh.a), 1ull << g1, 8ull, 1ull << hb};
+  cuuint64_t stride[4] = {16ull << sh.a, 16ull << sh.p, 16ull << (sh.p + g1), 16ull << (sh.p + sh.g)};
+  cuuint32_t box[5] = {2u << sh.a, 1u, 1u << g1, 1u, 1u};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dim, stride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        (CUtensorMapL2promotion)RSV_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace
 struct rsv_context;
 namespace {
-bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv::Shape& sh);
+bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv::Shape& sh, bool eighth = false);
 
 // Choose the tile-load mode of a pass and set its TMA descriptors (encoded once per vector and
 // shape, rsv_context::maps).
@@ -212,6 +229,29 @@ void set_tile_load(rsv_context* c, rsv::PassArgs& A) {
     // output tiles by TMA tensor stores through the same tile geometry
     if (A.out != nullptr && cached_tile_map(c, &A.tm_o, A.out, sh)) A.tstore = 1;
   }
+}
+
+// Peer-memory passes: partner tiles by TMA into the kernel's shared-memory ring when the pass has
+// full 4096-amplitude tiles, >= 8 amplitudes a thread and a TMA tile load (RSV_PEER_TMA=0 in the
+// environment keeps the per-thread P2P loads, for comparison).
+void set_peer_load(rsv_context* c, rsv::PassArgs& A) {
+  A.peer_tma = 0;
+  if (A.npeer == 0 || A.sh.a + A.sh.g != rsv::kLoBits) return;
+  static const bool off = [] {
+    const char* e = std::getenv("RSV_PEER_TMA");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (off) return;
+  if (A.kind != rsv::PASS_FIRST && A.kind != rsv::PASS_MID) return;
+  if ((1 << rsv::kLoBits) / rsv::pass_threads_for(rsv::kLoBits, A.kind, A.sh.a) < 8) return;
+  if (A.load == rsv::LOAD_CONTIG) {
+    A.peer_tma = 1;
+    return;
+  }
+  if (A.load != rsv::LOAD_TENSOR) return;
+  for (int g = 0; g < A.npeer; ++g)
+    if (!cached_tile_map(c, &A.tm_peer[g], A.peer[g], A.sh, true)) return;
+  A.peer_tma = 1;
 }
 
 struct PassPlan {
@@ -266,6 +306,7 @@ struct rsv_context {
   // peer-memory mode: the partner shards' slots mapped into this process (CUDA IPC / UVA);
   // peer_slots[g][physical slot] for global qubit g (empty: exchange through the callback)
   std::vector<std::vector<const cplx*>> peer_slots;
+  long long peer_passes[2] = {0, 0};   // peer-memory passes launched: TMA ring, per-thread loads
   bool reorth = false;              // full re-orthogonalisation (krylov.py:103-104), opt-in
   bool tail_regen = true;           // beyond the resident basis: ring + regeneration (else split in time)
   int speculate = -1;               // launch iteration j+1 before testing j: -1 auto (N <= 24), 0 off, 1 on
@@ -297,15 +338,16 @@ struct rsv_context {
 
 namespace {
 
-bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv::Shape& sh) {
+bool cached_tile_map(rsv_context* c, CUtensorMap* m, const void* base, const rsv::Shape& sh, bool eighth) {
+  const int gk = eighth ? -1 - sh.g : sh.g;   // eighth-tile maps keyed apart
   for (const auto& e : c->maps)
-    if (e.base == base && e.n == sh.n && e.a == sh.a && e.p == sh.p && e.g == sh.g) {
+    if (e.base == base && e.n == sh.n && e.a == sh.a && e.p == sh.p && e.g == gk) {
       *m = e.map;
       return true;
     }
-  if (!encode_tile_map(m, base, sh)) return false;
+  if (!(eighth ? encode_eighth_map(m, base, sh) : encode_tile_map(m, base, sh))) return false;
   if (c->maps.size() >= 512) c->maps.clear();   // user vectors of rsv_apply_hamiltonian come and go
-  c->maps.push_back({base, sh.n, sh.a, sh.p, sh.g, *m});
+  c->maps.push_back({base, sh.n, sh.a, sh.p, gk, *m});
   return true;
 }
 
@@ -924,6 +966,8 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     A.raw = (last && c->sharded) ? 1 : 0;
     A.mail = (last && !c->sharded) ? c->d_mail : nullptr;
     set_tile_load(c, A);
+    set_peer_load(c, A);
+    if (A.npeer > 0) ++c->peer_passes[A.peer_tma ? 0 : 1];
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));
     prof_end(c);
@@ -1699,6 +1743,13 @@ int rsv_enable_peer_access(const void* ptr) {
     return RSV_OK;
   }
   if (e != cudaSuccess) return fail(RSV_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d): %s", at.device, cudaGetErrorString(e));
+  return RSV_OK;
+}
+
+int rsv_shard_peer_stats(rsv_context* c, long long* out2) {
+  if (!c || !out2) return fail(RSV_ERR_ARG, "NULL argument");
+  out2[0] = c->peer_passes[0];
+  out2[1] = c->peer_passes[1];
   return RSV_OK;
 }
 

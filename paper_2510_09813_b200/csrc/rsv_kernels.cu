@@ -80,6 +80,9 @@ __device__ __forceinline__ void mbar_init_fence() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -519,8 +522,19 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 //   x ring : 2 stages, tile t+G is requested right after the tile-t barrier
 //   e buf  : this tile's elementwise operand, requested after the same barrier, awaited
 //            just before the epilogue
-template <int TB, int KIND, int NT, bool DIAG>
+// Peer-memory mode with PEER: the partner shards' tiles come by TMA over NVLink into a ring of
+// kPeerSlots shared-memory slots of one eighth of a tile (8 KB) each -- chunk c of the CTA's
+// sequence (tile it, eighth k, partner p) = it * 8 * npeer + k * npeer + p -- completed by
+// mbarriers (full: expected bytes; empty: every thread has read the slot). Thread 0 refills the
+// slot of chunk c-1 with chunk c-1+kPeerSlots while chunk c is consumed, so up to three chunks are
+// in flight; the partner reads take no LSU instructions and overlap the local flips.
+constexpr int kPeerSlots = 4;
+constexpr int kPeerChunk = (1 << kLoBits) / 8;   // amplitudes per slot
+constexpr size_t kPeerRingBytes = kPeerSlots * kPeerChunk * sizeof(cplx) + 2 * kPeerSlots * sizeof(uint64_t) + 128;
+
+template <int TB, int KIND, int NT, bool DIAG, bool PEER = false>
 __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
+  static_assert(!PEER || (TB == kLoBits && (1 << TB) / NT >= 8), "peer ring: full tiles, >= 8 amplitudes a thread");
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -533,6 +547,11 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
   cplx* ebuf = xbuf + 2 * TILE;                               // [TILE]
   double* rows = reinterpret_cast<double*>(ebuf + TILE);     // [2][16]
   uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 32);   // xbar[0], xbar[1], ebar
+  // peer ring (PEER): slots 128-byte aligned after the barriers, then full[4], empty[4]
+  cplx* pring = reinterpret_cast<cplx*>(smem_al + ((3 * TILE * sizeof(cplx) + 32 * sizeof(double) +
+                                                    4 * sizeof(uint64_t) + 127) & ~size_t(127)));
+  uint64_t* pfull = reinterpret_cast<uint64_t*>(pring + kPeerSlots * kPeerChunk);
+  uint64_t* pempty = pfull + kPeerSlots;
   __shared__ double red[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -578,13 +597,44 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
     }
   };
 
+  // peer chunks of this CTA: (tiles it owns) x 8 eighths x npeer partners
+  const int npeer = PEER ? A.npeer : 1;
+  const uint32_t pchunks = PEER ? (uint32_t)((ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0) * 8 *
+                                             (uint64_t)npeer) : 0u;
+  auto issue_peer = [&](uint32_t c) {   // thread 0: chunk c into slot c % kPeerSlots
+    const uint32_t per_tile = 8u * (uint32_t)npeer;
+    const uint64_t tt = blockIdx.x + (uint64_t)(c / per_tile) * G;
+    const uint32_t rem = c % per_tile;
+    const int k = (int)(rem / (uint32_t)npeer), pp = (int)(rem % (uint32_t)npeer);
+    const int slot = (int)(c % kPeerSlots);
+    mbar_arrive_expect_tx(&pfull[slot], kPeerChunk * sizeof(cplx));
+    if (A.load == LOAD_CONTIG) {
+      bulk_g2s(pring + slot * kPeerChunk, A.peer[pp] + tile_index(A.sh, tt, 0) + (uint64_t)k * kPeerChunk,
+               kPeerChunk * sizeof(cplx), &pfull[slot]);
+    } else {
+      const int m = A.sh.p - A.sh.a;
+      tma_load_5d(pring + slot * kPeerChunk, &A.tm_peer[pp], 0, (int)(tt & ((1ull << m) - 1ull)), 0, k,
+                  (int)(tt >> m), &pfull[slot]);
+    }
+  };
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
+    if (PEER) {
+      for (int s2 = 0; s2 < kPeerSlots; ++s2) {
+        mbar_init(&pfull[s2], 1);
+        mbar_init(&pempty[s2], NT);
+      }
+    }
     mbar_init_fence();
   }
   __syncthreads();
+  if constexpr (PEER) {
+    if (tid == 0)
+      for (uint32_t c = 0; c < pchunks && c < (uint32_t)kPeerSlots; ++c) issue_peer(c);
+  }
+  uint32_t pc = 0;                     // next peer chunk to consume
   unsigned xphase = 0u, ephase = 0u;   // bit s = parity of x stage s (a register, not a local array)
   // output tiles through the e buffer (in place over the operand) and a TMA store issued at the
   // next tile barrier (no per-thread global stores, no 64-bit address arithmetic per amplitude)
@@ -670,7 +720,32 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
     // sharded runs in peer-memory mode: the flips on the global qubits read the partner shards'
     // x (same local index) straight from their HBM over NVLink; they are part of this pass's
     // operator, so they also enter <x|A x> (alpha's partial share)
-    for (int g = 0; g < A.npeer; ++g) {
+    if constexpr (PEER) {
+      constexpr int EPK = EPT / 8;   // a thread's amplitudes per eighth: e = tid + NT * (k * EPK + ii)
+      #pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        for (int pp = 0; pp < npeer; ++pp, ++pc) {
+          const int slot = (int)(pc % kPeerSlots);
+          mbar_wait(&pfull[slot], (pc / kPeerSlots) & 1u);
+          const cplx* src = pring + slot * kPeerChunk + tid;
+          const double c = A.peer_coef[pp] * xs;
+          #pragma unroll
+          for (int ii = 0; ii < EPK; ++ii) {
+            const cplx v = src[ii * NT];
+            ac[k * EPK + ii].x = fma(c, v.x, ac[k * EPK + ii].x);
+            ac[k * EPK + ii].y = fma(c, v.y, ac[k * EPK + ii].y);
+          }
+          mbar_arrive(&pempty[slot]);
+          if (tid == 0 && pc >= 1 && pc - 1 + kPeerSlots < pchunks) {
+            // every thread has read chunk pc-1: its slot takes chunk pc-1+kPeerSlots
+            const uint32_t cp = pc - 1;
+            mbar_wait(&pempty[cp % kPeerSlots], (cp / kPeerSlots) & 1u);
+            issue_peer(cp + kPeerSlots);
+          }
+        }
+      }
+    }
+    for (int g = 0; g < (PEER ? 0 : A.npeer); ++g) {
       const cplx* pp = A.peer[g] + g0;
       const double c = A.peer_coef[g] * xs;
       cplx pv[EPT];
@@ -1067,10 +1142,10 @@ __device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
   }
 }
 
-template <int TB, int KIND, int NT, bool DIAG>
+template <int TB, int KIND, int NT, bool DIAG, bool PEER = false>
 __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2)
     pass_kernel_tma(const __grid_constant__ PassArgs A) {
-  pass_tma_body<TB, KIND, NT, DIAG>(A);
+  pass_tma_body<TB, KIND, NT, DIAG, PEER>(A);
 }
 template <int TB, int KIND, int NT, bool DIAG>
 __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2)
@@ -2019,6 +2094,22 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   }
 #endif
 #if RSV_TMA
+  if constexpr (TB == kLoBits && (KIND == PASS_FIRST || KIND == PASS_MID)) {
+    if (args.npeer > 0 && args.peer_tma) {   // partner tiles through the TMA ring
+      constexpr size_t smem_peer = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128 +
+                                   kPeerRingBytes;
+      if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
+        static int occ_p256 = 0;
+        return launch_persistent(pass_kernel_tma<TB, KIND, RSV_LAST_THREADS, DIAG, true>, args, args.sh.n_tiles,
+                                 RSV_LAST_THREADS, smem_peer, &occ_p256, st);
+      }
+      if constexpr (pass_threads(TB) != RSV_LAST_THREADS) {
+        static int occ_p = 0;
+        return launch_persistent(pass_kernel_tma<TB, KIND, pass_threads(TB), DIAG, true>, args, args.sh.n_tiles,
+                                 pass_threads(TB), smem_peer, &occ_p, st);
+      }
+    }
+  }
   if constexpr (TB >= 3) {
     constexpr size_t smem_tma = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
     if constexpr (TB == kLoBits && KIND == PASS_MID && RSV_LAST_THREADS != NT) {

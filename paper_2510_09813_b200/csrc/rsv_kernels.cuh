@@ -143,9 +143,12 @@ struct alignas(64) PassArgs {
   int j;                                // Lanczos iteration
   int qsweep;                           // LAST_LANCZOS: compute q_{j+1}
   int raw;                              // LAST_LANCZOS of a sharded run: store local sums (host all-reduces)
-  int npeer;                            // sharded, peer-memory mode (first pass): global-qubit flips
-  const cplx* peer[4];                  //   read the partner shards' x over NVLink (P2P loads)
+  int npeer;                            // sharded, peer-memory mode (passes before the last): global-qubit
+  const cplx* peer[4];                  //   flips read the partner shards' x over NVLink
   double peer_coef[4];                  //   Omega_g / 2
+  int peer_tma;                         // 1: partner tiles by TMA (bulk copy for LOAD_CONTIG, tm_peer for
+  CUtensorMap tm_peer[4];               //   LOAD_TENSOR: box = one eighth of the tile) into a shared-memory
+                                        //   ring; 0: per-thread P2P loads
   double* sc; double* part; unsigned* counter;
   double* mail;                         // LAST_LANCZOS (not raw): mapped pinned host memory receiving
                                         //   [n0sq (j=0)], alpha_j, beta_j -- the host reads them after the

@@ -22,6 +22,7 @@ top, so a sharded run is checked against the unsharded oracle.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -532,6 +533,13 @@ class FusedShardEngine:
     def state(self):
         return self.eng.state()
 
+    def peer_stats(self):
+        """Peer-memory passes launched so far: {"tma": partner tiles by TMA into the shared-memory
+        ring, "loads": per-thread P2P loads}."""
+        out = (ctypes.c_longlong * 2)()
+        self.nat.check(self.eng.lib.rsv_shard_peer_stats(self.eng.ctx, out))
+        return {"tma": int(out[0]), "loads": int(out[1])}
+
     def close(self):
         self.nat.check(self.eng.lib.rsv_set_shard_peers(self.eng.ctx, 0, None, 0))
         self.nat.check(self.eng.lib.rsv_set_shard(self.eng.ctx, self.nat.COMM_FN(), None, None))
@@ -572,5 +580,7 @@ def evolve_sv_sharded_fused(seq, reg, dist, tolerance=1e-10, max_krylov_dim=100,
         reps.append(rep)
     occ = eng.occupations()
     psi = eng.state().clone()
+    if info is not None:   # peer-memory passes: partner tiles by TMA ring / per-thread P2P loads
+        info["peer_passes"] = eng.peer_stats()
     eng.close()
     return psi, reps, occ

@@ -23,7 +23,9 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False):
+def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False, peer_tma=True):
+    if not peer_tma:   # per-thread P2P loads instead of the TMA ring (read once, when the context is made)
+        os.environ["RSV_PEER_TMA"] = "0"
     import torch
     import torch.distributed as dist
 
@@ -47,16 +49,19 @@ def _worker(rank, world, port, outdir, n, k0, steps, cap, peer=False):
         np.save(os.path.join(outdir, "occ.npy"), occ)
         np.save(os.path.join(outdir, "in.npy"), {"pos": list(reg.positions_um), "om": om, "de": de,
                                                  "iters": [r.iterations for r in reps],
-                                                 "sub": [r.substeps + r.regenerated for r in reps]}, allow_pickle=True)
+                                                 "sub": [r.substeps + r.regenerated for r in reps],
+                                                 "peer_passes": info.get("peer_passes")}, allow_pickle=True)
     dist.barrier()
     dist.destroy_process_group()
 
 
 @pytest.mark.timeout(400)
-@pytest.mark.parametrize("world,n,cap,peer", [(2, 14, None, False), (4, 14, None, False), (2, 17, None, False),
-                                              (2, 14, 6, False), (2, 17, None, True), (4, 16, None, True),
-                                              (2, 15, 6, True), (4, 24, None, True)])
-def test_fused_sharded_evolution(tmp_path, world, n, cap, peer):
+@pytest.mark.parametrize("world,n,cap,peer,peer_tma", [(2, 14, None, False, True), (4, 14, None, False, True),
+                                                       (2, 17, None, False, True), (2, 14, 6, False, True),
+                                                       (2, 17, None, True, True), (4, 16, None, True, True),
+                                                       (2, 15, 6, True, True), (4, 24, None, True, True),
+                                                       (2, 17, None, True, False), (4, 24, None, True, False)])
+def test_fused_sharded_evolution(tmp_path, world, n, cap, peer, peer_tma):
     # (4, 14): 12 local qubits -> one lo pass carries the diagonal, the shard offset and the q-sweep;
     # (2, 17): 16 local qubits -> lo + one group pass; cap 6 forces ring + regeneration across shards;
     # peer=True: peer-memory mode (the first passes read the partner shards' slots through CUDA IPC --
@@ -65,9 +70,15 @@ def test_fused_sharded_evolution(tmp_path, world, n, cap, peer):
     import torch.multiprocessing as mp
 
     k0, steps = 30, (4 if n < 20 else 1)   # the CPU oracle pays 2^n per H.psi with full re-orthogonalisation
-    mp.spawn(_worker, args=(world, _port(), str(tmp_path), n, k0, steps, cap, peer), nprocs=world, join=True)
+    # peer_tma: the partner tiles come by TMA (bulk copy / eighth-tile tensor map) into the pass kernels'
+    # shared-memory ring; False: per-thread P2P loads (RSV_PEER_TMA=0)
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path), n, k0, steps, cap, peer, peer_tma), nprocs=world,
+             join=True)
     psi = np.concatenate([np.load(tmp_path / f"s{r}.npy") for r in range(world)])
     inp = np.load(tmp_path / "in.npy", allow_pickle=True).item()
+    if peer:   # the requested partner-read mechanism really ran
+        pp = inp["peer_passes"]
+        assert (pp["tma"] > 0 and pp["loads"] == 0) if peer_tma else (pp["tma"] == 0 and pp["loads"] > 0), pp
     from paper_2510_09813_b200.workloads import C6_RB70
 
     u = O.interaction_matrix(inp["pos"], C6_RB70)
