@@ -404,8 +404,8 @@ def run_sharded(args, rank, world, local, pg):
     # self-check of the multi-GPU run: the communicator saw every rank, one GPU per rank, and the mode
     # (peer memory: TMA ring or P2P loads; or exchange) that actually ran
     devs = [None] * world
-    dist.all_gather_object(devs, (torch.cuda.current_device(), torch.cuda.get_device_properties(local).uuid.hex
-                                  if hasattr(torch.cuda.get_device_properties(local), "uuid") else str(local)))
+    props = torch.cuda.get_device_properties(local)
+    dist.all_gather_object(devs, (torch.cuda.current_device(), str(getattr(props, "uuid", local))))
     mg_check = {"backend": dist.get_backend(), "world": dist.get_world_size(), "requested": args.gpus,
                 "distinct_gpus": len({d[1] for d in devs}), "peer_memory": bool(peer_mode),
                 "peer_passes": peer_passes,   # partner tiles by TMA ring / per-thread P2P loads

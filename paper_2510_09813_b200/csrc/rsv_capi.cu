@@ -242,8 +242,8 @@ void set_peer_load(rsv_context* c, rsv::PassArgs& A) {
     return e != nullptr && e[0] == '0';
   }();
   if (off) return;
-  if (A.kind != rsv::PASS_FIRST && A.kind != rsv::PASS_MID) return;
-  if ((1 << rsv::kLoBits) / rsv::pass_threads_for(rsv::kLoBits, A.kind, A.sh.a) < 8) return;
+  if ((A.kind != rsv::PASS_FIRST && A.kind != rsv::PASS_MID) || A.npeer > 2) return;
+  if ((1 << rsv::kLoBits) / rsv::peer_pass_threads(A.kind, A.sh.a) < 8) return;
   if (A.load == rsv::LOAD_CONTIG) {
     A.peer_tma = 1;
     return;
@@ -967,6 +967,9 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
     A.mail = (last && !c->sharded) ? c->d_mail : nullptr;
     set_tile_load(c, A);
     set_peer_load(c, A);
+    // with the TMA ring the lo pass runs 256 threads x 16 amplitudes (the 512-thread variant spills
+    // under its 128-register cap); the kernel launcher picks the same count (rsv::peer_pass_threads)
+    if (A.peer_tma) A.fl = flips_for(p, omegas, rsv::peer_pass_threads(A.kind, A.sh.a));
     if (A.npeer > 0) ++c->peer_passes[A.peer_tma ? 0 : 1];
     prof_begin(c, family_of(pi, np));
     CUDA_TRY(rsv::launch_pass(A, c->st));

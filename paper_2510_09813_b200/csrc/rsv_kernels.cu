@@ -2,6 +2,7 @@
 #include "rsv_kernels.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 #ifndef RSV_STAGES
 #define RSV_STAGES 2
@@ -522,19 +523,23 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 //   x ring : 2 stages, tile t+G is requested right after the tile-t barrier
 //   e buf  : this tile's elementwise operand, requested after the same barrier, awaited
 //            just before the epilogue
-// Peer-memory mode with PEER: the partner shards' tiles come by TMA over NVLink into a ring of
+// Peer-memory mode with NPEER > 0 partners: their tiles come by TMA over NVLink into a ring of
 // kPeerSlots shared-memory slots of one eighth of a tile (8 KB) each -- chunk c of the CTA's
-// sequence (tile it, eighth k, partner p) = it * 8 * npeer + k * npeer + p -- completed by
-// mbarriers (full: expected bytes; empty: every thread has read the slot). Thread 0 refills the
-// slot of chunk c-1 with chunk c-1+kPeerSlots while chunk c is consumed, so up to three chunks are
-// in flight; the partner reads take no LSU instructions and overlap the local flips.
+// sequence (tile it, eighth k, partner p) = it * 8 * NPEER + k * NPEER + p -- completed by mbarriers
+// (full: expected bytes; empty: every thread has read the slot). The ring holds half a partner tile
+// (a quarter with two partners), so a tile's chunks are consumed at 2 * NPEER points spread over the
+// flip phase (before the flips, between them, in the epilogue), kPeerSlots chunks at each; thread 0
+// refills a slot as soon as every thread has read it, so the chunks of the next point land while
+// the flips in between run. The partner reads take no LSU instructions.
 constexpr int kPeerSlots = 4;
 constexpr int kPeerChunk = (1 << kLoBits) / 8;   // amplitudes per slot
 constexpr size_t kPeerRingBytes = kPeerSlots * kPeerChunk * sizeof(cplx) + 2 * kPeerSlots * sizeof(uint64_t) + 128;
 
-template <int TB, int KIND, int NT, bool DIAG, bool PEER = false>
+template <int TB, int KIND, int NT, bool DIAG, int NPEER = 0>
 __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
-  static_assert(!PEER || (TB == kLoBits && (1 << TB) / NT >= 8), "peer ring: full tiles, >= 8 amplitudes a thread");
+  constexpr bool PEER = NPEER > 0;
+  static_assert(NPEER <= 2 && (!PEER || (TB == kLoBits && (1 << TB) / NT >= 8)),
+                "peer ring: 1 or 2 partners, full tiles, >= 8 amplitudes a thread");
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -598,7 +603,7 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
   };
 
   // peer chunks of this CTA: (tiles it owns) x 8 eighths x npeer partners
-  const int npeer = PEER ? A.npeer : 1;
+  constexpr int npeer = PEER ? NPEER : 1;
   const uint32_t pchunks = PEER ? (uint32_t)((ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0) * 8 *
                                              (uint64_t)npeer) : 0u;
   auto issue_peer = [&](uint32_t c) {   // thread 0: chunk c into slot c % kPeerSlots
@@ -689,6 +694,37 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
       xv[i] = s[tid + i * NT];
       ac[i] = make_double2(0.0, 0.0);
     }
+    // partner chunks of consumption point Q: eighths [Q*E8, (Q+1)*E8) of every partner
+    constexpr int NPTS = 2 * npeer, E8 = 8 / NPTS, EPK = EPT / 8;
+    auto consume = [&](auto qc) {
+      constexpr int Q = decltype(qc)::value;
+      #pragma unroll
+      for (int k = Q * E8; k < (Q + 1) * E8; ++k) {
+        #pragma unroll
+        for (int pp = 0; pp < npeer; ++pp, ++pc) {
+          const int slot = (int)(pc % kPeerSlots);
+          mbar_wait(&pfull[slot], (pc / kPeerSlots) & 1u);
+          const cplx* src = pring + slot * kPeerChunk + tid;   // e = tid + NT (k EPK + ii)
+          const double c = A.peer_coef[pp] * xs;
+          #pragma unroll
+          for (int ii = 0; ii < EPK; ++ii) {
+            const cplx v = src[ii * NT];
+            ac[k * EPK + ii].x = fma(c, v.x, ac[k * EPK + ii].x);
+            ac[k * EPK + ii].y = fma(c, v.y, ac[k * EPK + ii].y);
+          }
+          mbar_arrive(&pempty[slot]);
+        }
+      }
+      // once every thread has read the point's last chunk it has read all kPeerSlots of them (in
+      // order): one wait, then each slot takes the chunk kPeerSlots ahead
+      if (tid == 0) {
+        const uint32_t last = pc - 1;
+        mbar_wait(&pempty[last % kPeerSlots], (last / kPeerSlots) & 1u);
+        for (uint32_t c = pc - kPeerSlots; c < pc; ++c)
+          if ((int64_t)pchunks - (int64_t)c > kPeerSlots) issue_peer(c + kPeerSlots);
+      }
+    };
+    if constexpr (PEER) consume(std::integral_constant<int, 0>{});
     #pragma unroll
     for (int b = 0; b < RB; ++b) {
       #pragma unroll
@@ -697,7 +733,17 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
         ac[i].y = fma(rc[b], xv[i ^ (1 << b)].y, ac[i].y);
       }
     }
+    if constexpr (NPEER == 2) {   // points 1 and 2 after a third and two thirds of the shared-memory flips
+      if (A.fl.count < 3) {
+        consume(std::integral_constant<int, 1>{});
+        consume(std::integral_constant<int, 2>{});
+      }
+    }
     for (int f = 0; f < A.fl.count; ++f) {
+      if constexpr (NPEER == 2) {
+        if (A.fl.count >= 3 && f == A.fl.count / 3) consume(std::integral_constant<int, 1>{});
+        if (A.fl.count >= 3 && f == (2 * A.fl.count) / 3) consume(std::integral_constant<int, 2>{});
+      }
       const cplx* ps = s + (tid ^ A.fl.mask[f]);
       const double c = A.fl.coef[f] * xs;
       #pragma unroll
@@ -707,6 +753,7 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
         ac[i].y = fma(c, p.y, ac[i].y);
       }
     }
+    if constexpr (PEER) consume(std::integral_constant<int, NPTS - 1>{});
     if (DIAG) {
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
@@ -720,31 +767,6 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
     // sharded runs in peer-memory mode: the flips on the global qubits read the partner shards'
     // x (same local index) straight from their HBM over NVLink; they are part of this pass's
     // operator, so they also enter <x|A x> (alpha's partial share)
-    if constexpr (PEER) {
-      constexpr int EPK = EPT / 8;   // a thread's amplitudes per eighth: e = tid + NT * (k * EPK + ii)
-      #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        for (int pp = 0; pp < npeer; ++pp, ++pc) {
-          const int slot = (int)(pc % kPeerSlots);
-          mbar_wait(&pfull[slot], (pc / kPeerSlots) & 1u);
-          const cplx* src = pring + slot * kPeerChunk + tid;
-          const double c = A.peer_coef[pp] * xs;
-          #pragma unroll
-          for (int ii = 0; ii < EPK; ++ii) {
-            const cplx v = src[ii * NT];
-            ac[k * EPK + ii].x = fma(c, v.x, ac[k * EPK + ii].x);
-            ac[k * EPK + ii].y = fma(c, v.y, ac[k * EPK + ii].y);
-          }
-          mbar_arrive(&pempty[slot]);
-          if (tid == 0 && pc >= 1 && pc - 1 + kPeerSlots < pchunks) {
-            // every thread has read chunk pc-1: its slot takes chunk pc-1+kPeerSlots
-            const uint32_t cp = pc - 1;
-            mbar_wait(&pempty[cp % kPeerSlots], (cp / kPeerSlots) & 1u);
-            issue_peer(cp + kPeerSlots);
-          }
-        }
-      }
-    }
     for (int g = 0; g < (PEER ? 0 : A.npeer); ++g) {
       const cplx* pp = A.peer[g] + g0;
       const double c = A.peer_coef[g] * xs;
@@ -1142,10 +1164,10 @@ __device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
   }
 }
 
-template <int TB, int KIND, int NT, bool DIAG, bool PEER = false>
+template <int TB, int KIND, int NT, bool DIAG, int NPEER = 0>
 __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2)
     pass_kernel_tma(const __grid_constant__ PassArgs A) {
-  pass_tma_body<TB, KIND, NT, DIAG, PEER>(A);
+  pass_tma_body<TB, KIND, NT, DIAG, NPEER>(A);
 }
 template <int TB, int KIND, int NT, bool DIAG>
 __global__ void __launch_bounds__(NT, (NT >= RSV_PASS_THREADS || NT == RSV_LAST_THREADS) ? 1 : 2)
@@ -2073,6 +2095,23 @@ cudaError_t launch_persistent(Kernel kern, const Args& args, uint64_t ntiles, in
   return cudaGetLastError();
 }
 
+template <int TB, int KIND, bool DIAG, int NPEER>
+cudaError_t launch_peer_pass(const PassArgs& args, cudaStream_t st) {
+  constexpr size_t smem_peer = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128 +
+                               kPeerRingBytes;
+  if (peer_pass_threads(KIND, args.sh.a) == RSV_LAST_THREADS) {
+    static int occ_p256 = 0;
+    return launch_persistent(pass_kernel_tma<TB, KIND, RSV_LAST_THREADS, DIAG, NPEER>, args, args.sh.n_tiles,
+                             RSV_LAST_THREADS, smem_peer, &occ_p256, st);
+  }
+  if constexpr (pass_threads(TB) != RSV_LAST_THREADS) {
+    static int occ_p = 0;
+    return launch_persistent(pass_kernel_tma<TB, KIND, pass_threads(TB), DIAG, NPEER>, args, args.sh.n_tiles,
+                             pass_threads(TB), smem_peer, &occ_p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int TB, int KIND, bool DIAG>
 cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   constexpr int NT = pass_threads(TB);
@@ -2095,19 +2134,9 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
 #endif
 #if RSV_TMA
   if constexpr (TB == kLoBits && (KIND == PASS_FIRST || KIND == PASS_MID)) {
-    if (args.npeer > 0 && args.peer_tma) {   // partner tiles through the TMA ring
-      constexpr size_t smem_peer = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128 +
-                                   kPeerRingBytes;
-      if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
-        static int occ_p256 = 0;
-        return launch_persistent(pass_kernel_tma<TB, KIND, RSV_LAST_THREADS, DIAG, true>, args, args.sh.n_tiles,
-                                 RSV_LAST_THREADS, smem_peer, &occ_p256, st);
-      }
-      if constexpr (pass_threads(TB) != RSV_LAST_THREADS) {
-        static int occ_p = 0;
-        return launch_persistent(pass_kernel_tma<TB, KIND, pass_threads(TB), DIAG, true>, args, args.sh.n_tiles,
-                                 pass_threads(TB), smem_peer, &occ_p, st);
-      }
+    if (args.npeer > 0 && args.npeer <= 2 && args.peer_tma) {   // partner tiles through the TMA ring
+      if (args.npeer == 1) return launch_peer_pass<TB, KIND, DIAG, 1>(args, st);
+      return launch_peer_pass<TB, KIND, DIAG, 2>(args, st);
     }
   }
   if constexpr (TB >= 3) {

@@ -64,6 +64,11 @@ constexpr int pass_threads_for(int tb, int kind, int a) {
   return ((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ? RSV_LAST_THREADS
                                                                                        : pass_threads(tb);
 }
+// Threads of a peer-memory pass with the TMA ring (full tiles): the lo pass too runs RSV_LAST_THREADS
+// (its contiguous tile puts a thread's amplitudes at one stride for any count).
+constexpr int peer_pass_threads(int kind, int a) {
+  return kind == 0 ? RSV_LAST_THREADS : pass_threads_for(kLoBits, kind, a);
+}
 #ifndef RSV_COMBINE_THREADS
 #define RSV_COMBINE_THREADS 512
 #endif
