@@ -852,7 +852,7 @@ bool fused_iteration(const rsv_context* c) {
   const PassPlan& lo = c->plan[0];
   const PassPlan& last = c->plan[1];
   if (!lo.lo || lo.chunk || lo.sh.a + lo.sh.g != rsv::kLoBits || last.sh.a + last.sh.g != rsv::kLoBits) return false;
-  if (last.sh.a > rsv::ilog2(RSV_LAST_THREADS)) return false;   // a thread's amplitudes at one stride
+  if (last.sh.a > rsv::ilog2(RSV_ITER2_THREADS)) return false;   // a thread's amplitudes at one stride
   return c->fuse > 0 || c->n <= kFuseMaxQubits;
 }
 
@@ -866,7 +866,7 @@ int launch_lanczos_iteration(rsv_context* c, int j, const double* omegas, const 
       const PassPlan& p = c->plan[pi];
       A.kind = pi == 0 ? rsv::PASS_FIRST : rsv::PASS_LAST_LANCZOS;
       A.sh = p.sh;
-      A.fl = flips_for(p, omegas, RSV_LAST_THREADS);
+      A.fl = flips_for(p, omegas, RSV_ITER2_THREADS);
       A.dg = diag_for(c, p, deltas);
       A.x = kvec(c, j);
       A.x_scale_slot = rsv::SC_SG + j;

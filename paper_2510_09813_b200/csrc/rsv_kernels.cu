@@ -1489,10 +1489,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 }
 
 template <bool DIAG>
-__global__ void __launch_bounds__(RSV_LAST_THREADS, 1) iter2_kernel(const __grid_constant__ Iter2Args A) {
-  pass_tma_body<kLoBits, PASS_FIRST, RSV_LAST_THREADS, DIAG>(A.lo);
+__global__ void __launch_bounds__(RSV_ITER2_THREADS, 1) iter2_kernel(const __grid_constant__ Iter2Args A) {
+  pass_tma_body<kLoBits, PASS_FIRST, RSV_ITER2_THREADS, DIAG>(A.lo);
   grid_barrier(A.gridbar);
-  pass_rot_body<kLoBits, PASS_LAST_LANCZOS, RSV_LAST_THREADS, false>(A.last);
+  pass_rot_body<kLoBits, PASS_LAST_LANCZOS, RSV_ITER2_THREADS, false>(A.last);
   // second arrival: the last CTA to get here resets the barrier for the next launch
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(A.gridbar, 1u) == 2u * gridDim.x - 1u) *A.gridbar = 0u;
@@ -2192,7 +2192,7 @@ cudaError_t launch_chunk_d(const ChunkArgs& args, cudaStream_t st) {
 
 template <bool DIAG>
 cudaError_t launch_iter2_d(const Iter2Args& args, cudaStream_t st) {
-  constexpr int NT = RSV_LAST_THREADS;
+  constexpr int NT = RSV_ITER2_THREADS;
   constexpr size_t smem = 3 * (1 << kLoBits) * sizeof(cplx) + 48 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
   auto kern = iter2_kernel<DIAG>;
   static int occ = 0;

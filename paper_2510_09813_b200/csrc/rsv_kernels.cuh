@@ -56,6 +56,10 @@ constexpr int pass_threads(int tb) { return (1 << tb) < RSV_PASS_THREADS ? (1 <<
 #define RSV_LAST_THREADS 256   // measured at N=29: last pass 5.16 -> 5.01 ms (4 register bits)
 #endif
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+// threads of the fused two-pass iteration kernel (iter2_kernel; registers of 16..21 qubits)
+#ifndef RSV_ITER2_THREADS
+#define RSV_ITER2_THREADS RSV_LAST_THREADS
+#endif
 // threads of the L2 chunk pass (its M tiles need 12 - gm <= log2 of this)
 #ifndef RSV_CHUNK_THREADS
 #define RSV_CHUNK_THREADS RSV_PASS_THREADS
