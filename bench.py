@@ -607,6 +607,11 @@ def run_ours(args):
                 "achieved_gbs": irreducible / (pass_total_ms / 1e3) / 1e9 if pass_total_ms else None,
                 "frac": (irreducible / (pass_total_ms / 1e3) / 1e9 / hbm_peak) if pass_total_ms else None,
                 "passes_bytes_per_amp": 48 * (len(plan) if plan else 1)}
+    # the plan's own bound: its passes move passes_bytes_per_amp, so at the copy peak the per-H.psi
+    # fraction cannot exceed 48 / passes_bytes_per_amp
+    per_hpsi["plan_bound_frac"] = 48.0 / per_hpsi["passes_bytes_per_amp"]
+    per_hpsi["frac_of_plan_bound"] = (per_hpsi["frac"] / per_hpsi["plan_bound_frac"]
+                                      if per_hpsi["frac"] is not None else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
