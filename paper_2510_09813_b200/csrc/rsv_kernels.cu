@@ -162,6 +162,47 @@ __device__ __forceinline__ uint64_t elem_offset(const Shape& sh, uint32_t e) {
   return (uint64_t)lo | (h << sh.p);
 }
 
+// Flips on a tile bit that is a lane bit of the thread layout (mask < 32) take the partner from the
+// neighbouring lane's registers by warp shuffles instead of a shared-memory load: 4 x SHFL.32 per
+// complex128 cost half the MIO/shared-memory-port time of one LDS.128 (tools/shfl_lds_bench.cu:
+// 243 vs 126 B/clk/SM; the two share the pipe), and the x tile is already in registers.
+// Measured at N=29 (profiles/r2_shfl_flips.md): slower in the mid pass (five of its eight shared-
+// memory flips are lane bits: the shuffles' issue slots and dependent latency outweigh the port time
+// they save) and the lo pass; in the last pass (one lane bit among four) 1.7 % faster on a
+// 1687 MHz box, 2 % slower on a 1537 MHz one. Off; RSV_SHFL_FLIPS=1 shuffles every lane bit in the
+// last pass (rotating-buffer body) and lane bits >= RSV_SHFL_TMA_MIN in the lo/mid passes.
+#ifndef RSV_SHFL_FLIPS
+#define RSV_SHFL_FLIPS 0
+#endif
+#ifndef RSV_SHFL_TMA_MIN
+#define RSV_SHFL_TMA_MIN 32
+#endif
+__device__ __forceinline__ cplx shfl_xor_c(cplx v, int m) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+// ac[i] += c * (partner of xv[i] across tile bit m), partners of lane bits by shuffles, the others
+// from the tile in shared memory (s: this thread's element 0)
+template <int NT, int EPT, int MMIN>
+__device__ __forceinline__ void flip_into(cplx (&ac)[EPT], const cplx (&xv)[EPT], const cplx* s, int tid, int m,
+                                          double c) {
+  if (RSV_SHFL_FLIPS && NT >= 32 && m >= MMIN && m < 32) {
+    #pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const cplx p = shfl_xor_c(xv[i], m);
+      ac[i].x = fma(c, p.x, ac[i].x);
+      ac[i].y = fma(c, p.y, ac[i].y);
+    }
+    return;
+  }
+  const cplx* ps = s + (tid ^ m);
+  #pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const cplx p = ps[i * NT];
+    ac[i].x = fma(c, p.x, ac[i].x);
+    ac[i].y = fma(c, p.y, ac[i].y);
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ double warp_sum(double v) {
   constexpr unsigned mask = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
@@ -744,14 +785,7 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
         if (A.fl.count >= 3 && f == A.fl.count / 3) consume(std::integral_constant<int, 1>{});
         if (A.fl.count >= 3 && f == (2 * A.fl.count) / 3) consume(std::integral_constant<int, 2>{});
       }
-      const cplx* ps = s + (tid ^ A.fl.mask[f]);
-      const double c = A.fl.coef[f] * xs;
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        const cplx p = ps[i * NT];
-        ac[i].x = fma(c, p.x, ac[i].x);
-        ac[i].y = fma(c, p.y, ac[i].y);
-      }
+      flip_into<NT, EPT, RSV_SHFL_TMA_MIN>(ac, xv, s, tid, A.fl.mask[f], A.fl.coef[f] * xs);
     }
     if constexpr (PEER) consume(std::integral_constant<int, NPTS - 1>{});
     if (DIAG) {
@@ -1010,16 +1044,7 @@ __device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
         ac[i].y = fma(rc[b], xv[i ^ (1 << b)].y, ac[i].y);
       }
     }
-    for (int f = 0; f < A.fl.count; ++f) {
-      const cplx* ps = s + (tid ^ A.fl.mask[f]);
-      const double c = A.fl.coef[f] * xs;
-      #pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        const cplx p = ps[i * NT];
-        ac[i].x = fma(c, p.x, ac[i].x);
-        ac[i].y = fma(c, p.y, ac[i].y);
-      }
-    }
+    for (int f = 0; f < A.fl.count; ++f) flip_into<NT, EPT, 1>(ac, xv, s, tid, A.fl.mask[f], A.fl.coef[f] * xs);
     if (DIAG) {
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
