@@ -913,7 +913,9 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
 // x(it); once every thread is past the flips (barrier B) it receives the operand of tile it+1, so
 // that load has a whole epilogue plus the next tile's flips to land; the operand buffer of tile it
 // receives x(it+2) after the next tile barrier (A). Cost: one more CTA barrier per tile.
-template <int TB, int KIND, int NT, bool DIAG>
+// X0: x of the CTA's first tile was already requested into buffer 0 (and the barriers initialised) by
+// rot_issue_x0 -- the fused iteration kernel does that before its grid barrier.
+template <int TB, int KIND, int NT, bool DIAG, bool X0 = false>
 __device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
@@ -988,7 +990,7 @@ __device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
     if (DIAG && tid == 0) bulk_g2s(rows + b * 16, A.dg.gc + tt * kGcStride, 112, &bars[b]);
   };
 
-  if (tid == 0) {
+  if (!X0 && tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
@@ -999,11 +1001,11 @@ __device__ __forceinline__ void pass_rot_body(const PassArgs& A) {
   const uint64_t t0 = blockIdx.x;
   if (t0 < ntiles) {   // prologue: x(0) -> buffer 0, operand(0) -> buffer 2
     if (tid == 0) {
-      mbar_arrive_expect_tx(&bars[0], x_bytes);
+      if (!X0) mbar_arrive_expect_tx(&bars[0], x_bytes);
       if (has_e) mbar_arrive_expect_tx(&bars[2], TILE * sizeof(cplx));
     }
     __syncthreads();
-    issue_x(t0, 0);
+    if (!X0) issue_x(t0, 0);
     if (has_e) issue(A.ein, &A.tm_e, t0, buf + 2 * TILE, &bars[2]);
   }
   int bx = 0;   // buffer of x(it); the operand of tile it sits in (bx + 2) % 3
@@ -1497,6 +1499,9 @@ __global__ void __launch_bounds__(NT, 1) chunk_kernel(const __grid_constant__ Ch
 }
 
 // ---------------------------------------------------------------- fused two-pass Lanczos iteration
+#ifndef RSV_ITER2_PREFETCH
+#define RSV_ITER2_PREFETCH 1
+#endif
 // Registers of 16..21 qubits have two passes per iteration (lo, last; 4096-amplitude tiles) over a state that lives in
 // L2; each pass is then a few tiles per SM, so launch latency, the pipeline fill and the tail of
 // the grid reduction are a large part of it. One cooperative launch runs both: the lo pass, a grid
@@ -1513,11 +1518,46 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   fence_proxy_async_smem();
 }
 
+// The last pass's first x tile (s_j, ready since the launch) is requested before the grid barrier,
+// so its load overlaps the wait for the other CTAs' lo tiles (contiguous / tensor-map tiles only).
+__device__ __forceinline__ bool rot_issue_x0(const PassArgs& A) {
+  if (A.load != LOAD_CONTIG && A.load != LOAD_TENSOR) return false;
+  constexpr int TILE = 1 << kLoBits;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  cplx* buf = reinterpret_cast<cplx*>(smem_al);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(buf + 3 * TILE) + 48);
+  __syncthreads();   // every thread is done with the lo pass's buffers
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    mbar_init_fence();
+    const uint64_t t0 = blockIdx.x;
+    if (t0 < A.sh.n_tiles) {
+      mbar_arrive_expect_tx(&bars[0], TILE * sizeof(cplx));
+      if (A.load == LOAD_CONTIG) {
+        bulk_g2s(buf, A.x + tile_index(A.sh, t0, 0), TILE * sizeof(cplx), &bars[0]);
+      } else {
+        const int m = A.sh.p - A.sh.a;
+        tma_load_5d(buf, &A.tm_x, 0, (int)(t0 & ((1ull << m) - 1ull)), 0, 0, (int)(t0 >> m), &bars[0]);
+      }
+    }
+  }
+  return true;
+}
+
 template <bool DIAG>
 __global__ void __launch_bounds__(RSV_ITER2_THREADS, 1) iter2_kernel(const __grid_constant__ Iter2Args A) {
   pass_tma_body<kLoBits, PASS_FIRST, RSV_ITER2_THREADS, DIAG>(A.lo);
+#if RSV_ITER2_PREFETCH
+  const bool x0 = rot_issue_x0(A.last);
+#else
+  const bool x0 = false;
+#endif
   grid_barrier(A.gridbar);
-  pass_rot_body<kLoBits, PASS_LAST_LANCZOS, RSV_ITER2_THREADS, false>(A.last);
+  if (x0) pass_rot_body<kLoBits, PASS_LAST_LANCZOS, RSV_ITER2_THREADS, false, true>(A.last);
+  else pass_rot_body<kLoBits, PASS_LAST_LANCZOS, RSV_ITER2_THREADS, false>(A.last);
   // second arrival: the last CTA to get here resets the barrier for the next launch
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(A.gridbar, 1u) == 2u * gridDim.x - 1u) *A.gridbar = 0u;
