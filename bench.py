@@ -491,7 +491,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     warm_ms = max_over_ranks(w0.elapsed_time(w1), pg)
     barrier(pg)
-    eng.set_profiling(True)
+    # per-kernel CUDA events around every launch at N >= 24; on smaller registers (host-paced ~35 us
+    # Lanczos iterations) every 16th launch per kernel family, the event pairs otherwise slow the
+    # timed loop itself (configs[1]: 16 %, tools/l20_overhead.py)
+    prof_every = 1 if n >= 24 else 16
+    eng.set_profiling(True, every=prof_every)
     sampler = ClockSampler(local)
     sampler.start()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -551,8 +555,10 @@ def run_ours(args):
     # ---- e2e through the public API: host initial state in, host final state + occupations out
     e2e = None
     if not args.no_e2e:
+        # the engine's blocks go back to torch's caching allocator, where evolve_sv's own engine
+        # finds them (no empty_cache: re-allocating the Krylov workspace from the driver cost
+        # ~0.5 s per call at configs[1], more than its whole 3 us sweep)
         del eng
-        torch.cuda.empty_cache()
         host_in = torch.zeros(2 ** n, dtype=torch.complex128, pin_memory=True)
         host_in[0] = 1.0
         host_out = torch.empty(2 ** n, dtype=torch.complex128, pin_memory=True)
@@ -643,7 +649,13 @@ def run_ours(args):
                 "timed_steps": f"{args.warmup + 1}..{total_steps}",
                 "diag": args.diag,
                 "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
-                "l2": "inputs larger than L2 (state = %.1f GB)" % (16 * 2 ** n / 1e9),
+                "l2": ("inputs larger than L2 (state = %.1f GB)" % (16 * 2 ** n / 1e9)
+                       if 3 * 16 * 2 ** n > 126e6 else
+                       "no flush: the state (%.1f MB) and an iteration's three vectors fit in the 126 MB L2 -- the "
+                       "configuration's own working set; the step's Krylov basis (%d vectors on average) does not"
+                       % (16 * 2 ** n / 1e6, round(k_avg))),
+                "kernel_timing": ("CUDA events around every launch" if prof_every == 1 else
+                                  f"CUDA events around every {prof_every}th launch per kernel family (mean x launches)"),
                 "pass_plan": plan,
                 "krylov_vectors_resident": krylov_cap,
             },

@@ -195,8 +195,11 @@ int rsv_set_reorthogonalize(rsv_context* ctx, int on);
  * handed out ahead of the first L tile (-1 = auto, 1.5 chunks). No reference counterpart: the reference
  * has one matvec loop (rydsim/_kernels.py:14). */
 int rsv_set_plan(rsv_context* ctx, int chunk_group_bits, long long chunk_lag);
+/* Kernel timing by CUDA events on the context's stream: 0 off, P >= 1 times one launch in P per kernel
+ * family (1: every launch). */
 int rsv_set_profiling(rsv_context* ctx, int on);
-/* per kernel family: [0]=lo pass, [1]=mid passes, [2]=last pass, [3]=combine; ms and launches */
+/* per kernel family: [0]=lo pass, [1]=mid passes, [2]=last pass, [3]=combine; ms (the mean of the timed
+ * launches times every launch) and launches */
 int rsv_get_profile(rsv_context* ctx, double* ms4, long long* launches4);
 int rsv_reset_profile(rsv_context* ctx);
 

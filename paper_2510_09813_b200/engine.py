@@ -221,8 +221,10 @@ class SvEngine(Context):
         return rep
 
     # -- profiling -----------------------------------------------------------------
-    def set_profiling(self, on: bool):
-        nat.check(self.lib.rsv_set_profiling(self.ctx, 1 if on else 0))
+    def set_profiling(self, on, every: int = 1):
+        """Kernel timing by CUDA events (profile()); ``every``: time one launch in that many per
+        kernel family (the per-launch event pair costs host time on small registers)."""
+        nat.check(self.lib.rsv_set_profiling(self.ctx, max(1, int(every)) if on else 0))
         nat.check(self.lib.rsv_reset_profile(self.ctx))
 
     def profile(self):
