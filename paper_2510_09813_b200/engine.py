@@ -112,6 +112,15 @@ class Context:
             pass
 
 
+def free_device_bytes(device) -> int:
+    """HBM a new workspace can take: the driver's free memory plus the blocks torch's caching
+    allocator holds that no tensor uses (an earlier engine's workspace: the allocator reuses them,
+    or releases them and retries when a request does not fit)."""
+    torch = _torch()
+    free, _total = torch.cuda.mem_get_info(device)
+    return int(free + torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device))
+
+
 def slots_that_fit(n_qubits: int, max_krylov_dim: int, diag: str, device, budget_bytes=None,
                    vector_cap=None) -> int:
     torch = _torch()
@@ -119,7 +128,7 @@ def slots_that_fit(n_qubits: int, max_krylov_dim: int, diag: str, device, budget
     want = min(int(max_krylov_dim), KMAX_NATIVE) + 1
     if vector_cap is not None:
         want = min(want, int(vector_cap) + 1)
-    free, _total = torch.cuda.mem_get_info(device)
+    free = free_device_bytes(device)
     extra = (8 << n_qubits) if diag == "vec" else 0
     avail = free - RESERVE_BYTES - extra
     if budget_bytes is not None:

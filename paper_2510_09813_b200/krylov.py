@@ -73,11 +73,10 @@ def _fused(slice_, psi, dt_ns, cfg):
     x, was_numpy = _as_device(psi)
     if tuple(x.shape) != (2 ** n,):
         raise ValidationError(f"state has shape {tuple(x.shape)}, expected ({2 ** n},)")
-    import torch
+    from .engine import free_device_bytes
 
     # leave room for the returned vector next to the workspace (at large N it takes all of HBM)
-    free, _total = torch.cuda.mem_get_info(x.device)
-    budget = max(0, free - (16 << n) - (1 << 30))
+    budget = max(0, free_device_bytes(x.device) - (16 << n) - (1 << 30))
     if slice_.structured:
         eng = SvEngine(n, slice_.interaction, diag="fly", max_krylov_dim=cfg.max_krylov_dim,
                        device=x.device, memory_budget_bytes=budget)

@@ -355,8 +355,9 @@ class FusedShardEngine:
         # a few GB: the Krylov slots otherwise take all of HBM
         dist.barrier()
         if memory_budget_bytes is None:
-            free, _total = torch.cuda.mem_get_info(dev)
-            memory_budget_bytes = max(0, free - (4 << 30))
+            from .engine import free_device_bytes
+
+            memory_budget_bytes = max(0, free_device_bytes(dev) - (4 << 30))
         # every rank must stop its Lanczos loop (and split a step) at the same Krylov cap, or the
         # shards would enter different collectives: agree on the smallest slot count that fits
         from .engine import slots_that_fit
