@@ -121,6 +121,8 @@ def cpu_baseline(n, seconds=12.0, chunk_log2=None, steps=None, warmup=1):
     from oracle import build as obuild
 
     lib = obuild.load()
+    # every host core this process may run on (torchrun sets OMP_NUM_THREADS=1 in each rank)
+    lib.svref_set_threads(len(os.sched_getaffinity(0)))
     dp = ctypes.POINTER(ctypes.c_double)
     avail = psutil.virtual_memory().available
     n_used = n
@@ -212,9 +214,10 @@ def barrier(pg):
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
-    rank, world, local, pg = dist_setup(args.gpus)
+    # CPU only: rank 0 alone runs it; the other ranks exit at once (no process group, no barrier),
+    # so none of them spins on a host core the reference's threads could use
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        barrier(pg)
         return 0
     t0 = time.time()
     steps = args.steps
@@ -245,7 +248,6 @@ def run_reference(args):
         "wall_s": time.time() - t0,
     }
     print(json.dumps(line), flush=True)
-    barrier(pg)
     return 0
 
 

@@ -37,6 +37,8 @@ def load():
     lib.svref_fill.argtypes = [ctypes.c_int64, dp, ctypes.c_uint64]
     lib.svref_fill.restype = None
     lib.svref_threads.restype = ctypes.c_int
+    lib.svref_set_threads.argtypes = [ctypes.c_int]
+    lib.svref_set_threads.restype = None
     lib.svref_zdotc.argtypes = [ctypes.c_int64, dp, dp, dp]
     lib.svref_zdotc.restype = None
     lib.svref_zaxpy.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_double, dp, dp]

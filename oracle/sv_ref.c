@@ -28,6 +28,16 @@ int svref_threads(void) {
 #endif
 }
 
+/* Threads of the parallel loops (the CPU baseline uses every core of its affinity mask, whatever
+ * OMP_NUM_THREADS a launcher such as torchrun has set). */
+void svref_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 void svref_matvec(int n, const double* psi, const double* diag, const double* half_omega, double* out) {
   const int64_t dim = (int64_t)1 << n;
 #pragma omp parallel for schedule(static)
