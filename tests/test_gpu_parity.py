@@ -327,6 +327,30 @@ class TestEvolve:
         assert np.array_equal(runs[0][0], runs[1][0])
         assert runs[0][1] == runs[1][1]
 
+    def test_sampled_kernel_timing(self, rs, torch):
+        # rsv_set_profiling(ctx, P) times one launch in P per kernel family: every launch is counted,
+        # the reported time is the timed launches' mean times the count, and the state is unchanged
+        from paper_2510_09813_b200.engine import SvEngine
+
+        rng = np.random.default_rng(77)
+        om, de, u = random_slice(rng, 18)
+        out = {}
+        for every in (1, 4):
+            e = SvEngine(18, u, krylov_vectors_cap=60)
+            e.set_profiling(True, every=every)
+            reps = [e.step(om, de, 5.0 + k, 1e-10, 100, next_params=(om, de)) for k in range(4)]
+            prof = e.profile()
+            out[every] = (e.state().cpu().numpy(), prof, sum(r.matvecs for r in reps))
+            e.close()
+        assert np.array_equal(out[1][0], out[4][0])
+        for every in (1, 4):
+            prof, mv = out[every][1], out[every][2]
+            first = next(iter(prof))
+            assert prof[first]["launches"] >= mv and prof[first]["ms"] > 0.0
+            assert prof["combine"]["launches"] >= 4   # + the first step's q_0 preparation
+        for fam in out[1][1]:
+            assert out[1][1][fam]["launches"] == out[4][1][fam]["launches"]
+
     @pytest.mark.parametrize("n", [16, 18, 21])
     def test_fused_iteration_matches_separate_passes(self, rs, torch, n):
         # [lo, last] plans with 4096-amplitude tiles (16..21 qubits) run each Lanczos iteration as one cooperative launch
