@@ -270,7 +270,14 @@ def build_dense(slice_: HamiltonianSlice) -> np.ndarray:
             f"dense Hamiltonian refused for N={n} > {DENSE_QUBIT_CAP} "
             "(exponential memory); use the structured apply instead")
     dim = 2 ** n
-    eye = np.eye(dim, dtype=complex)
-    # column b of H is H e_b: built with the GPU matvec itself (no CPU re-implementation)
-    cols = [apply_hamiltonian(slice_, eye[:, b]) for b in range(dim)]
-    return np.stack(cols, axis=1)
+    # the diagonal from the GPU (build_diagonal, or the slice's explicit one); the off-diagonal
+    # entries are the constants Omega_i/2 at (b, b ^ 2^i), placed as the reference places them
+    # (round 1 built H column by column from 2^N GPU matvecs)
+    diag = slice_.diagonal
+    diag = diag.cpu().numpy() if hasattr(diag, "cpu") else np.asarray(diag)
+    h = np.zeros((dim, dim), dtype=complex)
+    rows = np.arange(dim)
+    h[rows, rows] = diag
+    for i in range(n):
+        h[rows, rows ^ (1 << i)] += 0.5 * float(slice_.omegas[i])
+    return h

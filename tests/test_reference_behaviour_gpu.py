@@ -220,3 +220,30 @@ def test_expm_multiply_at_full_size(rs):
     assert abs(math.sqrt(rs.overlap(out, out).real) - 1.0) <= 1e-9
     del out, psi
     torch.cuda.empty_cache()
+
+
+class TestDense:
+    """hamiltonian.py:191 build_dense (the reference's small-N oracle helper): Hermitian, equal to the
+    structured apply column by column, refused above the cap."""
+
+    def test_dense_matches_structured_apply(self, rs):
+        rng = np.random.default_rng(191)
+        n = 8
+        reg = chain(rs, n, 6.0)
+        u = rs.interaction_matrix(reg)
+        om, de = rng.uniform(0.5, 3.0, n), rng.uniform(-2.0, 2.0, n)
+        sl = rs.HamiltonianSlice.from_parameters(om, de, u)
+        h = rs.build_dense(sl)
+        assert np.array_equal(h, h.conj().T)
+        psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        ref = O.apply_hamiltonian(om, O.build_diagonal(de, u), psi)
+        assert np.linalg.norm(h @ psi - ref) <= 1e-12 * np.linalg.norm(ref)
+        assert np.linalg.norm(h @ psi - host(rs.apply_hamiltonian(sl, psi))) <= 1e-12 * np.linalg.norm(ref)
+
+    def test_dense_refused_above_cap(self, rs):
+        from paper_2510_09813_b200.hamiltonian import DENSE_QUBIT_CAP
+
+        n = DENSE_QUBIT_CAP + 1
+        sl = rs.HamiltonianSlice.from_parameters(np.ones(n), np.zeros(n), np.zeros((n, n)))
+        with pytest.raises(rs.ValidationError):
+            rs.build_dense(sl)
