@@ -2206,7 +2206,8 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   }
   if constexpr (TB >= 3) {
     constexpr size_t smem_tma = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
-    if constexpr (TB == kLoBits && KIND == PASS_MID && RSV_LAST_THREADS != NT) {
+    if constexpr (TB == kLoBits && (KIND == PASS_MID || (RSV_LO_LAST_THREADS && KIND == PASS_FIRST)) &&
+                  RSV_LAST_THREADS != NT) {
       if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
         static int occ_mid = 0;
         return launch_persistent(pass_kernel_tma<TB, KIND, RSV_LAST_THREADS, DIAG>, args, args.sh.n_tiles,

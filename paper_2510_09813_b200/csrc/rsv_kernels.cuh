@@ -64,9 +64,17 @@ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 #ifndef RSV_CHUNK_THREADS
 #define RSV_CHUNK_THREADS RSV_PASS_THREADS
 #endif
+// the lo pass (PASS_FIRST, contiguous tile) with RSV_LAST_THREADS threads too: 16 amplitudes a thread,
+// 4 register bits, one shared-memory flip fewer per amplitude (measured at N=29 on a 1537 MHz box:
+// 4.04-4.06 -> 3.87 ms per launch, profiles/r2_last_pass.md); 0: 512 threads x 8 amplitudes
+#ifndef RSV_LO_LAST_THREADS
+#define RSV_LO_LAST_THREADS 1
+#endif
 constexpr int pass_threads_for(int tb, int kind, int a) {
-  return ((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ? RSV_LAST_THREADS
-                                                                                       : pass_threads(tb);
+  return (((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ||
+          (RSV_LO_LAST_THREADS && kind == 0 && tb == kLoBits))
+             ? RSV_LAST_THREADS
+             : pass_threads(tb);
 }
 // Threads of a peer-memory pass with the TMA ring (full tiles): the lo pass too runs RSV_LAST_THREADS
 // (its contiguous tile puts a thread's amplitudes at one stride for any count).
