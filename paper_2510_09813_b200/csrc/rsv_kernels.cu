@@ -569,9 +569,9 @@ __global__ void __launch_bounds__(NT, NT >= RSV_PASS_THREADS ? 1 : 2) pass_kerne
 // sequence (tile it, eighth k, partner p) = it * 8 * NPEER + k * NPEER + p -- completed by mbarriers
 // (full: expected bytes; empty: every thread has read the slot). The ring holds half a partner tile
 // (a quarter with two partners), so a tile's chunks are consumed at 2 * NPEER points spread over the
-// flip phase (before the flips, between them, in the epilogue), kPeerSlots chunks at each; thread 0
-// refills a slot as soon as every thread has read it, so the chunks of the next point land while
-// the flips in between run. The partner reads take no LSU instructions.
+// flip phase (before the flips, between them, in the epilogue), kPeerSlots chunks at each; once every
+// thread has read a point's last chunk, thread 0 refills all its slots, so the chunks of the next
+// point land while the flips in between run. The partner reads take no LSU instructions.
 constexpr int kPeerSlots = 4;
 constexpr int kPeerChunk = (1 << kLoBits) / 8;   // amplitudes per slot
 constexpr size_t kPeerRingBytes = kPeerSlots * kPeerChunk * sizeof(cplx) + 2 * kPeerSlots * sizeof(uint64_t) + 128;
