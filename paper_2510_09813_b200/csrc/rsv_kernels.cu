@@ -255,7 +255,7 @@ __device__ bool grid_finalize(const double (&mine)[NCOL], double* part, unsigned
 
 template <int EPT>
 struct RegBits {
-  static constexpr int value = EPT >= 16 ? 4 : (EPT >= 8 ? 3 : (EPT >= 4 ? 2 : (EPT >= 2 ? 1 : 0)));
+  static constexpr int value = EPT >= 32 ? 5 : (EPT >= 16 ? 4 : (EPT >= 8 ? 3 : (EPT >= 4 ? 2 : (EPT >= 2 ? 1 : 0))));
 };
 template <int N>
 struct Log2 {
@@ -581,6 +581,9 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
   constexpr bool PEER = NPEER > 0;
   static_assert(NPEER <= 2 && (!PEER || (TB == kLoBits && (1 << TB) / NT >= 8)),
                 "peer ring: 1 or 2 partners, full tiles, >= 8 amplitudes a thread");
+  // 32 amplitudes a thread (the 128-thread mid pass): outputs in two halves
+  constexpr bool SPLIT = (1 << TB) / NT == 32 && KIND == PASS_MID && !DIAG && !PEER;
+  static_assert(!SPLIT || !RSV_TSTORE_TMA, "the split mid pass stores by thread");
   constexpr int TILE = 1 << TB;
   constexpr int EPT = TILE / NT;
   constexpr int RB = RegBits<EPT>::value;
@@ -729,6 +732,66 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
     DiagRow<NT, EPT> dr;
     if (DIAG) dr.setup(A.dg, A.sh, t, tid, rows + stage * 16);
 
+    if constexpr (SPLIT) {
+      // 32 amplitudes a thread (5 register bits): all of x in registers, the outputs in two halves
+      // of 16 accumulators (half h = tile bit log2(NT)+4), so the register file holds 128 + 64
+      constexpr int H = EPT / 2;
+      cplx xv[EPT];
+      #pragma unroll
+      for (int i = 0; i < EPT; ++i) xv[i] = s[tid + i * NT];
+      cplx* po = A.out + g0;
+      #pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        cplx ac[H];
+        #pragma unroll
+        for (int ii = 0; ii < H; ++ii) ac[ii] = make_double2(0.0, 0.0);
+        #pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          #pragma unroll
+          for (int ii = 0; ii < H; ++ii) {
+            ac[ii].x = fma(rc[b], xv[(ii + h * H) ^ (1 << b)].x, ac[ii].x);
+            ac[ii].y = fma(rc[b], xv[(ii + h * H) ^ (1 << b)].y, ac[ii].y);
+          }
+        }
+        for (int f = 0; f < A.fl.count; ++f) {
+          const cplx* ps = s + (tid ^ A.fl.mask[f]) + h * H * NT;
+          const double c = A.fl.coef[f] * xs;
+          #pragma unroll
+          for (int ii = 0; ii < H; ++ii) {
+            const cplx p = ps[ii * NT];
+            ac[ii].x = fma(c, p.x, ac[ii].x);
+            ac[ii].y = fma(c, p.y, ac[ii].y);
+          }
+        }
+        for (int g = 0; g < A.npeer; ++g) {   // sharded, per-thread partner loads
+          const cplx* pp = A.peer[g] + g0 + (uint64_t)h * H * S;
+          const double c = A.peer_coef[g] * xs;
+          #pragma unroll
+          for (int ii = 0; ii < H; ++ii) {
+            const cplx v = __ldcg(pp + ii * S);
+            ac[ii].x = fma(c, v.x, ac[ii].x);
+            ac[ii].y = fma(c, v.y, ac[ii].y);
+          }
+        }
+        if (h == 0 && has_e) {
+          mbar_wait(&bars[2], ephase);
+          ephase ^= 1u;
+        }
+        #pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          const int i = ii + h * H;
+          double cr = ac[ii].x, ci = ac[ii].y;
+          acc_a = fma(xv[i].x, cr, fma(xv[i].y, ci, acc_a));
+          if (has_e) {
+            const cplx u = ebuf[tid + i * NT];
+            cr = fma(ecoef, u.x, cr);
+            ci = fma(ecoef, u.y, ci);
+          }
+          st_stream(po + i * S, make_double2(cr, ci));
+        }
+      }
+      continue;
+    }
     cplx xv[EPT], ac[EPT];
     #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -2206,6 +2269,14 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   }
   if constexpr (TB >= 3) {
     constexpr size_t smem_tma = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+    if constexpr (TB == kLoBits && KIND == PASS_MID && RSV_MID_THREADS != RSV_LAST_THREADS &&
+                  RSV_MID_THREADS != NT) {
+      if (pass_threads_for(TB, KIND, args.sh.a) == RSV_MID_THREADS) {
+        static int occ_mid128 = 0;
+        return launch_persistent(pass_kernel_tma<TB, KIND, RSV_MID_THREADS, DIAG>, args, args.sh.n_tiles,
+                                 RSV_MID_THREADS, smem_tma, &occ_mid128, st);
+      }
+    }
     if constexpr (TB == kLoBits && (KIND == PASS_MID || (RSV_LO_LAST_THREADS && KIND == PASS_FIRST)) &&
                   RSV_LAST_THREADS != NT) {
       if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {

@@ -70,16 +70,23 @@ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 #ifndef RSV_LO_LAST_THREADS
 #define RSV_LO_LAST_THREADS 1
 #endif
+// the mid passes with RSV_MID_THREADS: 128 threads x 32 amplitudes (5 register bits, computed in two
+// halves so that 32 amplitudes of x and 16 accumulators fit the register file) -- experiment switch
+#ifndef RSV_MID_THREADS
+#define RSV_MID_THREADS RSV_LAST_THREADS
+#endif
 constexpr int pass_threads_for(int tb, int kind, int a) {
-  return (((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ||
-          (RSV_LO_LAST_THREADS && kind == 0 && tb == kLoBits))
-             ? RSV_LAST_THREADS
-             : pass_threads(tb);
+  return (kind == 1 && tb == kLoBits && a <= ilog2c(RSV_MID_THREADS))
+             ? RSV_MID_THREADS
+             : (((kind == 3 || kind == 1) && tb == kLoBits && a <= ilog2c(RSV_LAST_THREADS)) ||
+                (RSV_LO_LAST_THREADS && kind == 0 && tb == kLoBits))
+                   ? RSV_LAST_THREADS
+                   : pass_threads(tb);
 }
 // Threads of a peer-memory pass with the TMA ring (full tiles): the lo pass too runs RSV_LAST_THREADS
 // (its contiguous tile puts a thread's amplitudes at one stride for any count).
 constexpr int peer_pass_threads(int kind, int a) {
-  return kind == 0 ? RSV_LAST_THREADS : pass_threads_for(kLoBits, kind, a);
+  return (kind == 0 || kind == 1) ? RSV_LAST_THREADS : pass_threads_for(kLoBits, kind, a);
 }
 #ifndef RSV_COMBINE_THREADS
 #define RSV_COMBINE_THREADS 512
@@ -120,7 +127,7 @@ struct FlipSet {
   int count;                // flips through shared memory (tile bit < log2(threads))
   int mask[kMaxFlips];      // tile-local bit masks
   double coef[kMaxFlips];   // Omega_q / 2
-  double rcoef[4];          // register flips: coefficient of tile bit log2(threads) + b (0 = inactive)
+  double rcoef[5];          // register flips: coefficient of tile bit log2(threads) + b (0 = inactive)
 };
 
 struct DiagArgs {
