@@ -252,7 +252,8 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-NCU_SUMMARIES = ("r2_ncu_n29_last_tstore.json",      # the last pass as it is now (TMA stores, round 2)
+NCU_SUMMARIES = ("r2_ncu_n29_final.json",            # round-2 HEAD: lo (256 threads), mid, last, combine
+                 "r2_ncu_n29_last_tstore.json",      # the last pass as it is now (TMA stores, round 2)
                  "r2_ncu_n29_before_tstore.json",    # lo / mid / combine (unchanged since)
                  "r1_ncu_n29_summary.json")
 
