@@ -377,6 +377,9 @@ cplx* kvec(const rsv_context* c, int i) { return slot(c, kidx(c, i)); }
 // runs last (it also carries the q-sweep). When a middle pass exists, the lowest qubits'
 // flips move from the lo pass (the heaviest: 12 flips + diagonal) to the first middle pass,
 // whose tile contains those bits too.
+#ifndef RSV_TOP_BIG
+#define RSV_TOP_BIG 0
+#endif
 #ifndef RSV_DELEGATE_LOW
 #define RSV_DELEGATE_LOW 3
 #endif
@@ -420,6 +423,9 @@ std::vector<PassPlan> hi_groups(int n, int from) {
   const int ng = (rem + gmax - 1) / gmax;
   std::vector<int> sizes;   // ascending: the top (most strided) groups are the smallest
   for (int i = 0; i < ng; ++i) sizes.push_back(rem / ng + (i >= ng - rem % ng ? 1 : 0));
+#if RSV_TOP_BIG
+  std::reverse(sizes.begin(), sizes.end());   // experiment: the top group takes the extra bit
+#endif
   std::vector<PassPlan> hi;
   int top = n;
   const int lt = rsv::ilog2(rsv::pass_threads(rsv::kLoBits));
