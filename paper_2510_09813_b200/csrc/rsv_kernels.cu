@@ -52,6 +52,9 @@
 #endif
 // tile barrier before the wait for x(t): the next tile's load is issued one wait earlier (measured
 // at N=29: no difference, lo/mid/last within 0.5 %; off)
+#ifndef RSV_DVEC_SMEM
+#define RSV_DVEC_SMEM 1   // diag="vec": stage the diagonal tile in shared memory by a bulk copy
+#endif
 #ifndef RSV_EARLY_X
 #define RSV_EARLY_X 0
 #endif
@@ -62,9 +65,18 @@ namespace {
 
 constexpr int kThreads = 256;     // generic / combine kernels
 
+#ifndef RSV_CP_L2PF
+#define RSV_CP_L2PF 0   // cp.async L2 prefetch-size hint (0: none, 128, 256 bytes)
+#endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+#if RSV_CP_L2PF == 256
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+#elif RSV_CP_L2PF == 128
+  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -601,6 +613,10 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
                                                     4 * sizeof(uint64_t) + 127) & ~size_t(127)));
   uint64_t* pfull = reinterpret_cast<uint64_t*>(pring + kPeerSlots * kPeerChunk);
   uint64_t* pempty = pfull + kPeerSlots;
+  // diag="vec": the tile's float64 diagonal entries arrive by one bulk copy at the tile barrier (bars[3]),
+  // where the peer ring would sit (never both); per-thread loads had exposed a DRAM latency per tile
+  const bool dvt = DIAG && !PEER && A.dvec_smem != 0;
+  const double* dbuf = reinterpret_cast<const double*>(pring);
   __shared__ double red[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -670,6 +686,7 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
+    if (dvt) mbar_init(&bars[3], 1);
     if (PEER) {
       for (int s2 = 0; s2 < kPeerSlots; ++s2) {
         mbar_init(&pfull[s2], 1);
@@ -685,6 +702,7 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
   }
   uint32_t pc = 0;                     // next peer chunk to consume
   unsigned xphase = 0u, ephase = 0u;   // bit s = parity of x stage s (a register, not a local array)
+  unsigned dphase = 0u;
   // output tiles through the e buffer (in place over the operand) and a TMA store issued at the
   // next tile barrier (no per-thread global stores, no 64-bit address arithmetic per amplitude)
   const bool tstore = RSV_TSTORE_TMA && A.tstore != 0;
@@ -723,6 +741,10 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
       if (!has_e) __syncthreads();
     }
     if (has_e) issue(A.ein, &A.tm_e, t, ebuf, &bars[2]);
+    if (dvt && tid == 0) {
+      mbar_arrive_expect_tx(&bars[3], TILE * sizeof(double));
+      bulk_g2s(const_cast<double*>(dbuf), A.dg.dvec + tile_index(A.sh, t, 0), TILE * sizeof(double), &bars[3]);
+    }
 #if RSV_EARLY_X
     // x(t) is awaited after the refills are issued: tile t+G's load starts one wait earlier
     mbar_wait(&bars[stage], (xphase >> stage) & 1u);
@@ -852,10 +874,15 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
     }
     if constexpr (PEER) consume(std::integral_constant<int, NPTS - 1>{});
     if (DIAG) {
+      if (dvt) {
+        mbar_wait(&bars[3], dphase);
+        dphase ^= 1u;
+      }
       #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         double d = dr.d[i];
-        if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+        if (dvt) d += dbuf[tid + i * NT];
+        else if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
         d *= xs;
         ac[i].x = fma(d, xv[i].x, ac[i].x);
         ac[i].y = fma(d, xv[i].y, ac[i].y);
@@ -922,7 +949,8 @@ __device__ __forceinline__ void pass_tma_body(const PassArgs& A) {
         }
         if (DIAG) {
           double d = dr.d[i];
-          if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
+          if (dvt) d += dbuf[tid + i * NT];
+          else if (A.dg.mode == DIAG_VEC) d += __ldcs(A.dg.dvec + g0 + i * S);
           hr = fma(d, ac[i].x, hr);
           hi = fma(d, ac[i].y, hi);
         }
@@ -2269,6 +2297,23 @@ cudaError_t launch_pass_tbkd(const PassArgs& args, cudaStream_t st) {
   }
   if constexpr (TB >= 3) {
     constexpr size_t smem_tma = 3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 128;
+    if constexpr (DIAG && TB == kLoBits) {
+      // diag="vec" on contiguous tiles: the diagonal tile is staged in shared memory (+32 KB)
+      if (args.dg.mode == DIAG_VEC && args.load == LOAD_CONTIG && RSV_DVEC_SMEM) {
+        constexpr size_t pring_off = (3 * (1 << TB) * sizeof(cplx) + 32 * sizeof(double) + 4 * sizeof(uint64_t) + 127) &
+                                     ~size_t(127);
+        constexpr size_t smem_dv = pring_off + (1 << TB) * sizeof(double) + 128;
+        PassArgs a2 = args;
+        a2.dvec_smem = 1;
+        if (pass_threads_for(TB, KIND, args.sh.a) == RSV_LAST_THREADS) {
+          static int occ_dv256 = 0;
+          return launch_persistent(pass_kernel_tma<TB, KIND, RSV_LAST_THREADS, DIAG>, a2, args.sh.n_tiles,
+                                   RSV_LAST_THREADS, smem_dv, &occ_dv256, st);
+        }
+        static int occ_dv = 0;
+        return launch_persistent(pass_kernel_tma<TB, KIND, NT, DIAG>, a2, args.sh.n_tiles, NT, smem_dv, &occ_dv, st);
+      }
+    }
     if constexpr (TB == kLoBits && KIND == PASS_MID && RSV_MID_THREADS != RSV_LAST_THREADS &&
                   RSV_MID_THREADS != NT) {
       if (pass_threads_for(TB, KIND, args.sh.a) == RSV_MID_THREADS) {

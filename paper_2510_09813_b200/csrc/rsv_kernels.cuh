@@ -177,6 +177,8 @@ struct alignas(64) PassArgs {
   double* mail;                         // LAST_LANCZOS (not raw): mapped pinned host memory receiving
                                         //   [n0sq (j=0)], alpha_j, beta_j -- the host reads them after the
                                         //   iteration's event, no device-to-host copies in the stream
+  int dvec_smem;                        // set by the launcher: diag="vec" tiles are staged in shared memory
+                                        //   by a bulk copy per tile (contiguous 4096-amplitude tiles)
 };
 
 struct CombineArgs {

@@ -64,6 +64,19 @@ class TestApplyHamiltonian:
             out = rs.apply_hamiltonian(s, g[f"n{n}_psi"])
             assert rel_err(out, g[f"n{n}_hpsi"]) <= 1e-12, n
 
+    @pytest.mark.parametrize("n", [14, 20, 23])
+    def test_explicit_diagonal_vec_mode_multi_pass(self, rs, torch, n):
+        # diag="vec" with a multi-pass plan: the lo pass (4096-amplitude contiguous tiles) stages the
+        # diagonal tile in shared memory by a bulk copy (RSV_DVEC_SMEM); against the oracle
+        rng = np.random.default_rng(500 + n)
+        om, de, u = random_slice(rng, n)
+        diag = O.build_diagonal(de, u)
+        psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        ref = O.apply_hamiltonian(om, diag, psi)
+        s = rs.HamiltonianSlice(om, diag)
+        out = rs.apply_hamiltonian(s, torch.from_numpy(psi).cuda()).cpu().numpy()
+        assert rel_err(out, ref) <= 1e-12
+
     @pytest.mark.parametrize("n", [14, 17, 20, 22, 23, 24])
     def test_multi_pass_against_oracle(self, rs, torch, n):
         # 13..22 qubits: lo pass + 1 group pass; >= 23: lo + 2 group passes
@@ -307,6 +320,29 @@ class TestEvolve:
         assert regen > 0
         assert rs.norm_difference(full.state(), capped.state()) <= 1e-12
         for e in (full, capped):
+            e.close()
+
+    @pytest.mark.parametrize("n", [22, 24])
+    def test_vec_diagonal_matches_fly(self, rs, torch, n):
+        # Lanczos steps with the precomputed interaction diagonal (lo pass reads it from shared memory,
+        # staged per tile) against the on-the-fly diagonal: same Krylov dimensions, same state to rounding
+        from paper_2510_09813_b200.engine import SvEngine
+
+        rng = np.random.default_rng(70 + n)
+        om, de, u = random_slice(rng, n)
+        engines = [SvEngine(n, u, diag=d, krylov_vectors_cap=40) for d in ("fly", "vec")]
+        psi0 = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+        psi0 /= np.linalg.norm(psi0)
+        for e in engines:
+            e.set_state(torch.from_numpy(psi0).cuda())
+            e.set_observables([1 << q for q in range(n)])
+        for k in range(3):
+            a, b = (e.step(om, de, 4.0 + k, 1e-10, 100, next_params=(om, de), observe=True) for e in engines)
+            assert a.iterations == b.iterations
+            assert abs(a.alpha0 - b.alpha0) <= 1e-11 * max(1.0, abs(a.alpha0))
+            assert np.abs(engines[0].observables() - engines[1].observables()).max() <= 1e-12
+        assert rs.norm_difference(engines[0].state(), engines[1].state()) <= 1e-11
+        for e in engines:
             e.close()
 
     @pytest.mark.parametrize("n", [10, 20])
